@@ -1,0 +1,159 @@
+/*
+ * slsp_b200.h — C ABI of the B200-native SlideSparse hot path.
+ *
+ * This is the drop-in boundary: plain pointers, sizes and a
+ * cudaStream_t, no C++ or torch types. Every entry point replaces one
+ * function of the reference's header-only C++ library (namespace slsp in
+ * /root/reference/proj/include/slsp/); the citation is given per function.
+ * The C++ drop-in headers in include/slsp/ are implemented on top of this
+ * ABI, and INTEGRATION.md shows the ctypes / C++ bindings.
+ *
+ * Conventions
+ *  - All data pointers are DEVICE pointers on the current device, except
+ *    where a parameter says "host". Buffers are caller-allocated; the library
+ *    keeps no pointer past the call (reference value semantics).
+ *  - Calls are stream-ordered on `stream`. Entry points that report data
+ *    errors (non-compliant weights, non-finite activations) take a device
+ *    scratch `status_ws` of SLSP_STATUS_WS_BYTES bytes; when it is non-NULL
+ *    the call synchronises `stream` and returns the error with its location,
+ *    mirroring the reference's exceptions. When NULL the check is skipped
+ *    (the hot path) and the call is fully asynchronous.
+ *  - Row-major everywhere. "Lifted width" kp is the padded width of the
+ *    lifted/slided K dimension: kp >= K' = ceil(K/l)*(l-2)/2*4, kp % 8 == 0
+ *    for the MMA-ready formats, kp % 256 == 0 for the GEMM entry points.
+ *    Padding windows hold zero values and the canonical codes (0,1).
+ *  - The library fails loudly: a missing device, wrong architecture or a
+ *    CUDA error is returned as SLSP_ERR_CUDA; there is no CPU fallback.
+ */
+#ifndef SLSP_B200_H
+#define SLSP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define SLSP_API __attribute__((visibility("default")))
+#else
+#define SLSP_API
+#endif
+
+typedef struct CUstream_st* slsp_stream_t; /* == cudaStream_t */
+
+/* Element types (weights / activations). */
+enum {
+  SLSP_DT_I8 = 0,   /* int8 two's complement                          */
+  SLSP_DT_BF16 = 1, /* bfloat16 bit patterns                          */
+  SLSP_DT_E4M3 = 2, /* fp8 e4m3fn codes (fp8.hpp)                     */
+  SLSP_DT_F32 = 3,
+  SLSP_DT_F64 = 4
+};
+
+/* Activation quantization kinds (quantize.hpp:16 QuantKind). */
+enum { SLSP_QUANT_INT8 = 0, SLSP_QUANT_FP8E4M3 = 1 };
+
+/* GEMM output modes. */
+enum {
+  SLSP_OUT_RAW_NM = 0,   /* accumulators, N x M (int32 for I8, fp32 otherwise) — gemm.hpp:214 */
+  SLSP_OUT_BF16_NM = 1,  /* bf16((acc*s_ch[n])*s_tok[t]), N x M                                */
+  SLSP_OUT_BF16_MN = 2   /* same values, M x N (token-major, what the next layer consumes)     */
+};
+
+/* Status codes; the C++ shim maps each to the reference's exception type. */
+enum {
+  SLSP_OK = 0,
+  SLSP_ERR_NOT_COMPLIANT = 1, /* slsp::NotCompliantError       (pattern.hpp:40) */
+  SLSP_ERR_DIMENSION = 2,     /* slsp::DimensionMismatchError  (pattern.hpp:43) */
+  SLSP_ERR_PLAN = 3,          /* AlreadyCompliant / NonIntegralWindowCount / InsufficientCapacity */
+  SLSP_ERR_NON_FINITE = 4,    /* slsp::NonFiniteInputError     (pattern.hpp:49) */
+  SLSP_ERR_INVALID = 5,       /* std::invalid_argument / std::overflow_error    */
+  SLSP_ERR_MALFORMED = 6,     /* slsp::MalformedMetadataError  (pattern.hpp:46) */
+  SLSP_ERR_UNSUPPORTED = 7,   /* shape/type outside what the sm_100a kernels handle */
+  SLSP_ERR_CUDA = 8           /* CUDA runtime/driver failure, no device, wrong arch */
+};
+
+#define SLSP_STATUS_WS_BYTES 64
+
+/* Version / diagnostics. */
+SLSP_API int slsp_version(void);
+SLSP_API const char* slsp_status_string(int status);
+/* Last CUDA error text seen by this thread (for SLSP_ERR_CUDA). */
+SLSP_API const char* slsp_last_cuda_error(void);
+/* 1 if device `dev` is an sm_100 part the kernels run on, else 0. */
+SLSP_API int slsp_device_supported(int dev);
+
+/* a1 — pattern.hpp:107-154 plan_status + plan_decomposition (host only).
+ * Hardware window fixed at hw_m:hw_n. Fills window_count and up to `cap`
+ * window starts. */
+SLSP_API int slsp_plan_decomposition(int z, int l, int hw_m, int hw_n, int* window_count, int* window_starts,
+                            int cap);
+
+/* a3/a4 — pack.hpp:171-204 pack_matrix. W (rows x cols, dtype) -> slided
+ * (rows x K', same dtype), K' = cols/l*wc*4. cols % l != 0 -> DIMENSION.
+ * Errors: NOT_COMPLIANT with (*err_row, *err_block) of the lowest row. */
+SLSP_API int slsp_pack_matrix(int dtype, const void* w, int64_t rows, int64_t cols, int z, int l, void* slided,
+                     void* status_ws, int64_t* err_row, int64_t* err_block, slsp_stream_t stream);
+
+/* a5 — gemm.hpp:70-110 compress. slided (rows x cols_exp) -> values
+ * (rows x cols_exp/2, dtype) + codes (rows x cols_exp/2 bytes, one 2-bit
+ * position per byte, the reference's in-memory format). */
+SLSP_API int slsp_compress(int dtype, const void* slided, int64_t rows, int64_t cols_exp, void* values, uint8_t* codes,
+                  void* status_ws, int64_t* err_row, int64_t* err_window, slsp_stream_t stream);
+
+/* a3+a4+a5 fused, the offline packer Φ in MMA-ready form:
+ *   values: rows x kp/2 (dtype), meta: rows x kp/8 bytes, four 2-bit codes per
+ *   byte LSB-first (== container.hpp:330-336 pack_codes per row == the 2:4
+ *   sparse-MMA metadata nibbles). cols need not be a multiple of l: the tail
+ *   block is zero-padded like quantize.hpp:130,162 does for activations. */
+SLSP_API int slsp_pack_compress(int dtype, const void* w, int64_t rows, int64_t cols, int z, int l, int64_t kp,
+                       void* values, uint8_t* meta, void* status_ws, int64_t* err_row, int64_t* err_block,
+                       slsp_stream_t stream);
+
+/* a8 — pack.hpp:238-261 magnitude_prune (synthesises compliant weights). */
+SLSP_API int slsp_magnitude_prune(int dtype, const void* w, int64_t rows, int64_t cols, int z, int l, void* out,
+                         slsp_stream_t stream);
+
+/* a12 — quantize.hpp:122-174 fused_quant_slide. x (rows x cols, F32|BF16)
+ * -> payload (rows x kp/4 uint32 words; word j = window j, byte d = position
+ * d, pack_word :91-94) + scales (rows, fp32). kp >= K' and kp % 4 == 0;
+ * kp == K' reproduces QuantizedLiftedActivation::payload exactly. */
+SLSP_API int slsp_fused_quant_slide(int in_dtype, const void* x, int64_t rows, int64_t cols, int z, int l, int kind,
+                           int64_t kp, uint32_t* payload, float* scales, void* status_ws, int64_t* bad_row,
+                           slsp_stream_t stream);
+
+/* a8 — quantize.hpp:52-68 quantize_row for every token row (the dense
+ * GEMM's activations): out rows x kpad bytes (zero padded), scales fp32. */
+SLSP_API int slsp_quantize_rows(int in_dtype, const void* x, int64_t rows, int64_t cols, int kind, int64_t kpad,
+                       uint8_t* out, float* scales, void* status_ws, int64_t* bad_row, slsp_stream_t stream);
+
+/* a9 — quantize.hpp:72-89 lift_row per token row (gemm.hpp:240-256
+ * lift_activations with tokens as rows). Pure gather, any dtype; cols % l == 0;
+ * out rows x kp (zero padded past K'). */
+SLSP_API int slsp_lift_rows(int dtype, const void* x, int64_t rows, int64_t cols, int z, int l, int64_t kp, void* out,
+                   slsp_stream_t stream);
+
+/* a13/a14 — gemm.hpp:164-233 sparse_gemm on tcgen05.mma.sp (sm_100a).
+ *   dtype I8  : values int8,  act = quantized payload bytes (int8), acc int32
+ *   dtype E4M3: values e4m3,  act = e4m3 payload bytes,              acc fp32
+ *   dtype BF16: values bf16,  act = lifted bf16,                     acc fp32
+ * values: n x kp/2, meta: n x kp/8 (slsp_pack_compress format), act: m x kp.
+ * kp % 256 == 0. s_ch (n) / s_tok (m) are required for the BF16 outputs.
+ * out: SLSP_OUT_RAW_NM / BF16_NM -> n x m (row stride ldo elements);
+ *      SLSP_OUT_BF16_MN -> m x n (row stride ldo). */
+SLSP_API int slsp_sparse_gemm(int dtype, const void* values, const uint8_t* meta, int64_t n, int64_t kp, const void* act,
+                     int64_t m, const float* s_ch, const float* s_tok, int out_mode, void* out, int64_t ldo,
+                     slsp_stream_t stream);
+
+/* a15 — gemm.hpp:142-162 dense_gemm on tcgen05.mma (the speedup
+ * denominator). w: n x k, act: m x k (token rows; the reference's X is k x m,
+ * the C++ shim transposes), k % 128 == 0. Outputs as slsp_sparse_gemm. */
+SLSP_API int slsp_dense_gemm(int dtype, const void* w, int64_t n, int64_t k, const void* act, int64_t m,
+                    const float* s_ch, const float* s_tok, int out_mode, void* out, int64_t ldo,
+                    slsp_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SLSP_B200_H */

@@ -1,0 +1,348 @@
+"""ctypes binding of the C ABI (include/slsp_b200.h) over torch device tensors.
+
+This is the Python host side of the drop-in boundary. Every function takes
+and returns CUDA tensors and calls exactly one ``slsp_*`` C entry point; the
+library is ``paper_2603_05232_b200/libslsp_b200.so`` (built in-tree by
+``paper_2603_05232_b200/build.py``). There is no CPU fallback: if the library
+or a B200 is missing, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from dataclasses import dataclass
+from pathlib import Path
+
+import torch
+
+LIB_PATH = Path(__file__).resolve().parent / "libslsp_b200.so"
+
+# ---- constants mirrored from include/slsp_b200.h -----------------------------
+DT_I8, DT_BF16, DT_E4M3, DT_F32, DT_F64 = 0, 1, 2, 3, 4
+QUANT_INT8, QUANT_FP8E4M3 = 0, 1
+OUT_RAW_NM, OUT_BF16_NM, OUT_BF16_MN = 0, 1, 2
+OK, ERR_NOT_COMPLIANT, ERR_DIMENSION, ERR_PLAN, ERR_NON_FINITE, ERR_INVALID, ERR_MALFORMED, \
+    ERR_UNSUPPORTED, ERR_CUDA = range(9)
+STATUS_WS_BYTES = 64
+
+
+# ---- error hierarchy (pattern.hpp:24-57) -------------------------------------
+class SlspError(RuntimeError):
+    """slsp::Error"""
+
+
+class NotCompliantError(SlspError):
+    pass
+
+
+class DimensionMismatchError(SlspError):
+    pass
+
+
+class PlanError(SlspError):
+    """AlreadyCompliantError / NonIntegralWindowCountError / InsufficientCapacityError."""
+
+
+class NonFiniteInputError(SlspError):
+    pass
+
+
+class MalformedMetadataError(SlspError):
+    pass
+
+
+class UnsupportedError(SlspError):
+    pass
+
+
+class CudaError(SlspError):
+    pass
+
+
+_ERRORS = {
+    ERR_NOT_COMPLIANT: NotCompliantError,
+    ERR_DIMENSION: DimensionMismatchError,
+    ERR_PLAN: PlanError,
+    ERR_NON_FINITE: NonFiniteInputError,
+    ERR_INVALID: ValueError,
+    ERR_MALFORMED: MalformedMetadataError,
+    ERR_UNSUPPORTED: UnsupportedError,
+    ERR_CUDA: CudaError,
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib() -> C.CDLL:
+    """Loads the native library (fails loudly; there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2603_05232_b200.build` "
+                                  "(the B200 path has no CPU fallback)")
+            L = C.CDLL(str(LIB_PATH))
+            i64, vp, i32 = C.c_int64, C.c_void_p, C.c_int
+            sigs = {
+                "slsp_version": (i32, []),
+                "slsp_status_string": (C.c_char_p, [i32]),
+                "slsp_last_cuda_error": (C.c_char_p, []),
+                "slsp_device_supported": (i32, [i32]),
+                "slsp_plan_decomposition": (i32, [i32, i32, i32, i32, vp, vp, i32]),
+                "slsp_pack_matrix": (i32, [i32, vp, i64, i64, i32, i32, vp, vp, vp, vp, vp]),
+                "slsp_compress": (i32, [i32, vp, i64, i64, vp, vp, vp, vp, vp, vp]),
+                "slsp_pack_compress": (i32, [i32, vp, i64, i64, i32, i32, i64, vp, vp, vp, vp, vp, vp]),
+                "slsp_magnitude_prune": (i32, [i32, vp, i64, i64, i32, i32, vp, vp]),
+                "slsp_fused_quant_slide": (i32, [i32, vp, i64, i64, i32, i32, i32, i64, vp, vp, vp, vp, vp]),
+                "slsp_quantize_rows": (i32, [i32, vp, i64, i64, i32, i64, vp, vp, vp, vp, vp]),
+                "slsp_lift_rows": (i32, [i32, vp, i64, i64, i32, i32, i64, vp, vp]),
+                "slsp_sparse_gemm": (i32, [i32, vp, vp, i64, i64, vp, i64, vp, vp, i32, vp, i64, vp]),
+                "slsp_dense_gemm": (i32, [i32, vp, i64, i64, vp, i64, vp, vp, i32, vp, i64, vp]),
+            }
+            for name, (res, args) in sigs.items():
+                fn = getattr(L, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = L
+    return _lib
+
+
+def _check(status: int, what: str, msg: str | None = None) -> None:
+    if status == OK:
+        return
+    cls = _ERRORS.get(status, SlspError)
+    text = msg or f"{what}: {lib().slsp_status_string(status).decode()}"
+    if status == ERR_CUDA:
+        text += f" ({lib().slsp_last_cuda_error().decode()})"
+    raise cls(text)
+
+
+def _ptr(t: torch.Tensor | None):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(device: torch.device | None = None):
+    return C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _status_ws(device) -> torch.Tensor:
+    return torch.empty(STATUS_WS_BYTES, dtype=torch.uint8, device=device)
+
+
+_DT_OF = {torch.int8: DT_I8, torch.bfloat16: DT_BF16, torch.uint8: DT_E4M3, torch.float32: DT_F32,
+          torch.float64: DT_F64, torch.float8_e4m3fn: DT_E4M3}
+
+
+def dtype_code(t: torch.Tensor) -> int:
+    try:
+        return _DT_OF[t.dtype]
+    except KeyError:
+        raise TypeError(f"unsupported element type {t.dtype}") from None
+
+
+def _raw(t: torch.Tensor) -> torch.Tensor:
+    """fp8 tensors travel as their uint8 codes."""
+    return t.view(torch.uint8) if t.dtype == torch.float8_e4m3fn else t
+
+
+def _require_cuda(*ts: torch.Tensor) -> None:
+    for t in ts:
+        if t is not None and (not t.is_cuda or not t.is_contiguous()):
+            raise ValueError("slsp_b200 operates on contiguous CUDA tensors")
+
+
+# ---- a1: geometry --------------------------------------------------------------
+def plan_decomposition(z: int, l: int, hw_m: int = 2, hw_n: int = 4) -> tuple[int, list[int]]:
+    """pattern.hpp:131-154 -> (window_count, window_starts)."""
+    wc = C.c_int(0)
+    starts = (C.c_int * 64)()
+    _check(lib().slsp_plan_decomposition(z, l, hw_m, hw_n, C.byref(wc), starts, 64), "plan_decomposition")
+    return wc.value, list(starts[: wc.value])
+
+
+def lifted_width(cols: int, z: int, l: int) -> int:
+    """K' = ceil(cols/l) * wc * 4 (quantize.hpp:130-133)."""
+    wc, _ = plan_decomposition(z, l)
+    return -(-cols // l) * wc * 4
+
+
+def round_up(x: int, a: int) -> int:
+    return -(-x // a) * a
+
+
+# ---- a3-a5: packer -----------------------------------------------------------
+def pack_matrix(w: torch.Tensor, z: int, l: int) -> torch.Tensor:
+    """pack.hpp:171-204 pack_matrix -> slided rows x K' (same dtype)."""
+    _require_cuda(w)
+    rows, cols = w.shape
+    wc, _ = plan_decomposition(z, l)
+    if cols % l:
+        raise DimensionMismatchError(f"matrix cols {cols} not divisible by block length {l}")
+    out = torch.empty((rows, cols // l * wc * 4), dtype=w.dtype, device=w.device)
+    er, eb = C.c_int64(-1), C.c_int64(-1)
+    st = lib().slsp_pack_matrix(dtype_code(w), _ptr(_raw(w)), rows, cols, z, l, _ptr(_raw(out)),
+                                _ptr(_status_ws(w.device)), C.byref(er), C.byref(eb), _stream(w.device))
+    _check(st, "pack_matrix", f"row {er.value}, block {eb.value} violates pattern {z}:{l}"
+           if st == ERR_NOT_COMPLIANT else None)
+    return out
+
+
+def compress(slided: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+    """gemm.hpp:70-110 compress -> (values rows x K'/2, codes rows x K'/2 bytes)."""
+    _require_cuda(slided)
+    rows, cexp = slided.shape
+    values = torch.empty((rows, cexp // 2), dtype=slided.dtype, device=slided.device)
+    codes = torch.empty((rows, cexp // 2), dtype=torch.uint8, device=slided.device)
+    er, ew = C.c_int64(-1), C.c_int64(-1)
+    st = lib().slsp_compress(dtype_code(slided), _ptr(_raw(slided)), rows, cexp, _ptr(_raw(values)), _ptr(codes),
+                             _ptr(_status_ws(slided.device)), C.byref(er), C.byref(ew), _stream(slided.device))
+    _check(st, "compress", f"window ({er.value}, {ew.value}) holds more than 2 nonzeros"
+           if st == ERR_NOT_COMPLIANT else None)
+    return values, codes
+
+
+@dataclass
+class PackedWeights:
+    """MMA-ready compressed weights: values n x kp/2, meta n x kp/8 (2-bit codes)."""
+    values: torch.Tensor
+    meta: torch.Tensor
+    n: int
+    k: int
+    kp: int
+    z: int
+    l: int
+
+    @property
+    def dtype(self) -> int:
+        return dtype_code(self.values)
+
+
+def pack_compress(w: torch.Tensor, z: int, l: int, kp: int | None = None, check: bool = True) -> PackedWeights:
+    """Fused Φ: pack_matrix + compress + pack_codes straight into the sparse-MMA format."""
+    _require_cuda(w)
+    rows, cols = w.shape
+    kprime = lifted_width(cols, z, l)
+    kp = round_up(kprime, 256) if kp is None else kp
+    values = torch.empty((rows, kp // 2), dtype=w.dtype, device=w.device)
+    meta = torch.empty((rows, kp // 8), dtype=torch.uint8, device=w.device)
+    er, eb = C.c_int64(-1), C.c_int64(-1)
+    ws = _status_ws(w.device) if check else None
+    st = lib().slsp_pack_compress(dtype_code(w), _ptr(_raw(w)), rows, cols, z, l, kp, _ptr(_raw(values)),
+                                  _ptr(meta), _ptr(ws), C.byref(er), C.byref(eb), _stream(w.device))
+    _check(st, "pack_compress", f"row {er.value}, block {eb.value} violates pattern {z}:{l}"
+           if st == ERR_NOT_COMPLIANT else None)
+    return PackedWeights(values, meta, rows, cols, kp, z, l)
+
+
+def magnitude_prune(w: torch.Tensor, z: int, l: int) -> torch.Tensor:
+    """pack.hpp:238-261 magnitude_prune."""
+    _require_cuda(w)
+    out = torch.empty_like(w)
+    _check(lib().slsp_magnitude_prune(dtype_code(w), _ptr(_raw(w)), w.shape[0], w.shape[1], z, l, _ptr(_raw(out)),
+                                      _stream(w.device)), "magnitude_prune")
+    return out
+
+
+# ---- a6-a12: activations -----------------------------------------------------------
+def _in_dtype(x: torch.Tensor) -> int:
+    if x.dtype == torch.float32:
+        return DT_F32
+    if x.dtype == torch.bfloat16:
+        return DT_BF16
+    raise TypeError(f"activations must be float32 or bfloat16, got {x.dtype}")
+
+
+def fused_quant_slide(x: torch.Tensor, z: int, l: int, kind: int = QUANT_INT8, kp: int | None = None,
+                      check: bool = True) -> tuple[torch.Tensor, torch.Tensor]:
+    """quantize.hpp:122-174 -> (payload rows x kp/4 uint32 words as int32 storage, scales fp32)."""
+    _require_cuda(x)
+    rows, cols = x.shape
+    kprime = lifted_width(cols, z, l)
+    kp = round_up(kprime, 256) if kp is None else kp
+    payload = torch.empty((rows, kp // 4), dtype=torch.int32, device=x.device)
+    scales = torch.empty(rows, dtype=torch.float32, device=x.device)
+    bad = C.c_int64(-1)
+    ws = _status_ws(x.device) if check else None
+    st = lib().slsp_fused_quant_slide(_in_dtype(x), _ptr(x), rows, cols, z, l, kind, kp, _ptr(payload),
+                                      _ptr(scales), _ptr(ws), C.byref(bad), _stream(x.device))
+    _check(st, "fused_quant_slide", f"non-finite activation value in row {bad.value}"
+           if st == ERR_NON_FINITE else None)
+    return payload, scales
+
+
+def quantize_rows(x: torch.Tensor, kind: int = QUANT_INT8, kpad: int | None = None,
+                  check: bool = True) -> tuple[torch.Tensor, torch.Tensor]:
+    """quantize.hpp:52-68 quantize_row for every token row -> (bytes rows x kpad, scales)."""
+    _require_cuda(x)
+    rows, cols = x.shape
+    kpad = round_up(cols, 128) if kpad is None else kpad
+    out = torch.empty((rows, kpad), dtype=torch.uint8, device=x.device)
+    scales = torch.empty(rows, dtype=torch.float32, device=x.device)
+    bad = C.c_int64(-1)
+    ws = _status_ws(x.device) if check else None
+    st = lib().slsp_quantize_rows(_in_dtype(x), _ptr(x), rows, cols, kind, kpad, _ptr(out), _ptr(scales),
+                                  _ptr(ws), C.byref(bad), _stream(x.device))
+    _check(st, "quantize_rows", f"non-finite activation value in row {bad.value}"
+           if st == ERR_NON_FINITE else None)
+    return out, scales
+
+
+def lift_rows(x: torch.Tensor, z: int, l: int, kp: int | None = None) -> torch.Tensor:
+    """quantize.hpp:72-89 lift_row per token row (bf16/fp32 passthrough)."""
+    _require_cuda(x)
+    rows, cols = x.shape
+    kprime = lifted_width(cols, z, l)
+    kp = kprime if kp is None else kp
+    out = torch.empty((rows, kp), dtype=x.dtype, device=x.device)
+    _check(lib().slsp_lift_rows(dtype_code(x), _ptr(x), rows, cols, z, l, kp, _ptr(out), _stream(x.device)),
+           "lift_rows")
+    return out
+
+
+# ---- a13-a15: GEMMs ------------------------------------------------------------------
+def _gemm_out(out_mode: int, n: int, m: int, acc_int: bool, device, out: torch.Tensor | None):
+    if out is not None:
+        return out
+    if out_mode == OUT_RAW_NM:
+        return torch.empty((n, m), dtype=torch.int32 if acc_int else torch.float32, device=device)
+    if out_mode == OUT_BF16_NM:
+        return torch.empty((n, m), dtype=torch.bfloat16, device=device)
+    return torch.empty((m, n), dtype=torch.bfloat16, device=device)
+
+
+def sparse_gemm(w: PackedWeights, act: torch.Tensor, s_ch: torch.Tensor | None = None,
+                s_tok: torch.Tensor | None = None, out_mode: int = OUT_RAW_NM,
+                out: torch.Tensor | None = None) -> torch.Tensor:
+    """gemm.hpp:199-233 on tcgen05.mma.sp. act: m x kp bytes (or the uint32 payload)."""
+    _require_cuda(act, s_ch, s_tok)
+    m = act.shape[0]
+    if act.shape[1] * act.element_size() != w.kp * w.values.element_size():
+        raise DimensionMismatchError("lifted activation width does not match compressed weights")
+    o = _gemm_out(out_mode, w.n, m, w.values.dtype == torch.int8, act.device, out)
+    ldo = o.shape[1]
+    _check(lib().slsp_sparse_gemm(w.dtype, _ptr(_raw(w.values)), _ptr(w.meta), w.n, w.kp, _ptr(act), m, _ptr(s_ch),
+                                  _ptr(s_tok), out_mode, _ptr(o), ldo, _stream(act.device)), "sparse_gemm")
+    return o
+
+
+def dense_gemm(w: torch.Tensor, act: torch.Tensor, s_ch: torch.Tensor | None = None,
+               s_tok: torch.Tensor | None = None, out_mode: int = OUT_RAW_NM,
+               out: torch.Tensor | None = None) -> torch.Tensor:
+    """gemm.hpp:142-162 on tcgen05.mma. w: n x k, act: m x k (token rows)."""
+    _require_cuda(w, act, s_ch, s_tok)
+    n, k = w.shape
+    m = act.shape[0]
+    if act.shape[1] * act.element_size() != k * w.element_size():
+        raise DimensionMismatchError("dense_gemm: W.cols must equal X.rows")
+    o = _gemm_out(out_mode, n, m, w.dtype == torch.int8, act.device, out)
+    ldo = o.shape[1]
+    _check(lib().slsp_dense_gemm(dtype_code(w), _ptr(_raw(w)), n, k, _ptr(act), m, _ptr(s_ch), _ptr(s_tok),
+                                 out_mode, _ptr(o), ldo, _stream(act.device)), "dense_gemm")
+    return o
+
+
+def device_supported(dev: int = 0) -> bool:
+    return bool(lib().slsp_device_supported(dev))

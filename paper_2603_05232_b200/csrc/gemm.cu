@@ -1,0 +1,460 @@
+// Structured-sparse and dense GEMMs on sm_100a 5th-gen tensor cores
+// (SURVEY.md §8a rows a13-a15, a18).
+//
+//   Y[n][t] = sum_k W[n][k] * X[t][k]       (gemm.hpp:142-233 orientation)
+//
+// One persistent kernel template, warp-specialised, CTA pair (cluster of 2,
+// tcgen05 cta_group::2):
+//   warp 0      TMA producer (both CTAs): A (weights, compressed for .sp),
+//               B (lifted activations), E (2-bit metadata) into a STAGES-deep
+//               smem ring; completion bytes land on the leader's barrier.
+//   warp 1      leader CTA: one elected thread issues tcgen05.cp (E -> TMEM)
+//               and tcgen05.mma[.sp] (M=256 across the pair, N=BN tokens);
+//               both CTAs: TMEM allocation.
+//   warps 2-5   epilogue (both CTAs): tcgen05.ld the accumulator lanes,
+//               optional per-channel x per-token dequant to BF16, stores.
+// Accumulators are double-buffered in TMEM so the epilogue of tile i overlaps
+// the mainloop of tile i+1. The weight (sparse) operand is A: MMA-M = output
+// features, MMA-N = tokens.
+#include <cstdio>
+#include <mutex>
+#include <unordered_map>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace {
+
+using namespace slsp_dev;
+
+constexpr int kNumThreads = 192;
+constexpr int kEpiWarp0 = 2;
+
+template <bool SPARSE_, MmaKind KIND_, int BN_, int STAGES_, int OUT_>
+struct Cfg {
+  static constexpr bool SPARSE = SPARSE_;
+  static constexpr MmaKind KIND = KIND_;
+  static constexpr int BN = BN_;          // tokens per pair tile (MMA N)
+  static constexpr int STAGES = STAGES_;
+  static constexpr int OUT = OUT_;
+  static constexpr int BM = 256;          // weight rows per pair tile (MMA M)
+  static constexpr int A_ROWS = 128;      // per CTA
+  static constexpr int B_ROWS = BN / 2;   // tokens per CTA
+  static constexpr int A_STAGE = 128 * 128;                  // one 128B-swizzle atom column
+  static constexpr int B_ATOMS = SPARSE ? 2 : 1;             // B bytes per stage = 2x A bytes for .sp
+  static constexpr int B_ATOM = B_ROWS * 128;
+  static constexpr int B_STAGE = B_ATOM * B_ATOMS;
+  static constexpr int E_STAGE = SPARSE ? 2 * 128 * 16 : 0;  // two 128x128b metadata atoms
+  static constexpr int STAGE_TX = A_STAGE + B_STAGE + E_STAGE;
+  static constexpr int K_BYTES_B = 128 * B_ATOMS;            // activation bytes consumed per stage
+  static constexpr int MMAS = 4;                             // per stage
+  static constexpr int ACC_COLS = BN;                        // 32-bit TMEM columns per accumulator
+  static constexpr int E_COL = 2 * BN;                       // metadata columns after both accumulators
+  static constexpr int TMEM_COLS = 512;
+  static_assert(!SPARSE || E_COL + 8 <= TMEM_COLS, "TMEM budget: 2 accumulators + metadata");
+  static_assert(SPARSE || 2 * BN <= TMEM_COLS, "TMEM budget: 2 accumulators");
+  static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "cta_group::2 N");
+  static constexpr int OFF_A = 0;
+  static constexpr int OFF_B = OFF_A + STAGES * A_STAGE;
+  static constexpr int OFF_E = OFF_B + STAGES * B_STAGE;
+  static constexpr int OFF_BAR = OFF_E + STAGES * E_STAGE;
+  static constexpr int NUM_BARS = 2 * STAGES + 4;
+  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16 + 1024;  // + alignment slack
+  static constexpr uint32_t C_FMT = KIND == MmaKind::I8 ? 2u : 1u;
+  static constexpr uint32_t AB_FMT = KIND == MmaKind::F8 ? 0u : 1u;
+  static constexpr uint32_t IDESC = make_idesc(SPARSE, C_FMT, AB_FMT, AB_FMT, BM, BN);
+  using Acc = typename std::conditional<KIND == MmaKind::I8, int32_t, float>::type;
+};
+
+struct Params {
+  int64_t n, m;       // weight rows, tokens
+  int num_kb;         // k-blocks (stages) per tile
+  int m_tiles, n_tiles;
+  const float* s_ch;  // per weight row
+  const float* s_tok; // per token
+  void* out;
+  int64_t ldo;
+};
+
+SLSP_DEVINL void tile_coords(int tile, int m_tiles, int n_tiles, int& mt, int& nt) {
+  constexpr int kGroup = 8;  // weight tiles per raster band (B reuse through L2)
+  const int per_group = kGroup * n_tiles;
+  const int g = tile / per_group;
+  const int first = g * kGroup;
+  const int gsize = min(kGroup, m_tiles - first);
+  const int r = tile - g * per_group;
+  mt = first + r % gsize;
+  nt = r / gsize;
+}
+
+template <typename C>
+SLSP_DEVINL void epilogue_store(const Params& p, const uint32_t (&r)[32], int64_t row, int64_t t0) {
+  using Acc = typename C::Acc;
+  if (row >= p.n) return;
+  const int valid = static_cast<int>(imin64(32, p.m - t0));
+  if (valid <= 0) return;
+  if constexpr (C::OUT == SLSP_OUT_RAW_NM) {
+    uint32_t* dst = reinterpret_cast<uint32_t*>(p.out) + row * p.ldo + t0;
+    if (valid == 32 && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        reinterpret_cast<uint4*>(dst)[i] = make_uint4(r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
+    } else {
+      for (int i = 0; i < valid; ++i) dst[i] = r[i];
+    }
+  } else {
+    const float sc = __ldg(p.s_ch + row);
+    float y[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      float a;
+      if constexpr (std::is_same<Acc, int32_t>::value) a = __int2float_rn(static_cast<int32_t>(r[i]));
+      else a = __uint_as_float(r[i]);
+      const float st = (t0 + i < p.m) ? __ldg(p.s_tok + t0 + i) : 0.f;
+      y[i] = __fmul_rn(__fmul_rn(a, sc), st);
+    }
+    if constexpr (C::OUT == SLSP_OUT_BF16_NM) {
+      __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.out) + row * p.ldo + t0;
+      if (valid == 32 && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          uint32_t w[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            __nv_bfloat162 h = __floats2bfloat162_rn(y[8 * i + 2 * j], y[8 * i + 2 * j + 1]);
+            w[j] = *reinterpret_cast<uint32_t*>(&h);
+          }
+          reinterpret_cast<uint4*>(dst)[i] = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      } else {
+        for (int i = 0; i < valid; ++i) dst[i] = __float2bfloat16_rn(y[i]);
+      }
+    } else {  // SLSP_OUT_BF16_MN: lanes hold consecutive features -> coalesced per token
+      __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.out) + t0 * p.ldo + row;
+      for (int i = 0; i < valid; ++i) dst[i * p.ldo] = __float2bfloat16_rn(y[i]);
+    }
+  }
+}
+
+template <typename C>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmE, const Params p) {
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem + C::OFF_A;
+  uint8_t* sB = smem + C::OFF_B;
+  uint8_t* sE = smem + C::OFF_E;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t warp = threadIdx.x >> 5;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cluster_id = blockIdx.x >> 1;
+  const int num_clusters = gridDim.x >> 1;
+  const int num_tiles = p.m_tiles * p.n_tiles;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 2 * 4);  // 4 epilogue warps in each CTA of the pair
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane_id() == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    if (C::SPARSE) tma_prefetch(&tmE);
+  }
+  if (warp == 1) tmem_alloc<2>(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer ----
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
+        int mt, nt;
+        tile_coords(tile, p.m_tiles, p.n_tiles, mt, nt);
+        const int a_row = mt * C::BM + static_cast<int>(rank) * C::A_ROWS;
+        const int b_row = nt * C::BN + static_cast<int>(rank) * C::B_ROWS;
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_TX);
+          const uint32_t bar = mapa_shared(smem_u32(&full[stage]), 0);
+          tma_load_2d_cg2(sA + stage * C::A_STAGE, &tmA, bar, kb * 128, a_row);
+#pragma unroll
+          for (int at = 0; at < C::B_ATOMS; ++at)
+            tma_load_2d_cg2(sB + stage * C::B_STAGE + at * C::B_ATOM, &tmB, bar, kb * C::K_BYTES_B + at * 128,
+                            b_row);
+          if constexpr (C::SPARSE) tma_load_3d_cg2(sE + stage * C::E_STAGE, &tmE, bar, 0, a_row, kb * 2);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer ----
+    if (leader && elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem + acc * C::ACC_COLS;
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(sA + stage * C::A_STAGE);
+          const uint32_t b_base = smem_u32(sB + stage * C::B_STAGE);
+          if constexpr (C::SPARSE) {
+            const uint32_t e_base = smem_u32(sE + stage * C::E_STAGE);
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+              tmem_cp_128x128b_cg2(tmem + C::E_COL + 4 * c, smem_desc(e_base + c * 2048, 2048, 128, 0));
+          }
+#pragma unroll
+          for (int j = 0; j < C::MMAS; ++j) {
+            const uint64_t adesc = smem_desc(a_base + j * 32, 16, 1024, 2);
+            const uint32_t acc_flag = (kb | j) != 0;
+            if constexpr (C::SPARSE) {
+              const uint64_t bdesc = smem_desc(b_base + (j >> 1) * C::B_ATOM + (j & 1) * 64, 16, 1024, 2);
+              umma_sparse_cg2<C::KIND>(d_tmem, adesc, bdesc, tmem + C::E_COL + 2 * j, C::IDESC, acc_flag);
+            } else {
+              const uint64_t bdesc = smem_desc(b_base + j * 32, 16, 1024, 2);
+              umma_dense_cg2<C::KIND>(d_tmem, adesc, bdesc, C::IDESC, acc_flag);
+            }
+          }
+          tc_commit_mc(&empty[stage], 0x3);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit_mc(&tfull[acc], 0x3);
+      }
+    }
+  } else {
+    // ------------------------------------------------ epilogue ----
+    const uint32_t quarter = warp & 3;  // TMEM lane quarter this warp may access
+    const uint32_t lane = lane_id();
+    int it = 0;
+    for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
+      int mt, nt;
+      tile_coords(tile, p.m_tiles, p.n_tiles, mt, nt);
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int64_t row = static_cast<int64_t>(mt) * C::BM + rank * C::A_ROWS + quarter * 32 + lane;
+      const uint32_t t_base = tmem + ((quarter * 32) << 16) + acc * C::ACC_COLS;
+#pragma unroll 1
+      for (int c = 0; c < C::BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(t_base + c * 32, r);
+        tmem_ld_wait();
+        epilogue_store<C>(p, r, row, static_cast<int64_t>(nt) * C::BN + c * 32);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc<2>(tmem, C::TMEM_COLS);
+#endif
+}
+
+// ---------------------------------------------------------------- host --
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// Byte-addressed 2D map (uint8 elements): rows x row_bytes, box rows x 128 B, 128B swizzle.
+int make_map_2d(CUtensorMap* map, const void* base, uint64_t row_bytes, uint64_t rows, uint32_t box_rows) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return SLSP_ERR_CUDA;
+  cuuint64_t dims[2] = {row_bytes, rows};
+  cuuint64_t strides[1] = {row_bytes};
+  cuuint32_t box[2] = {128, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? SLSP_OK : SLSP_ERR_CUDA;
+}
+
+// Metadata map: meta is rows x (kp/8) bytes. Viewed as (16 B, rows, kp/128)
+// so one box {16, 128, 2} lands as two canonical 128x16B UTCCP atoms.
+int make_map_meta(CUtensorMap* map, const void* base, uint64_t rows, uint64_t kp) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return SLSP_ERR_CUDA;
+  cuuint64_t dims[3] = {16, rows, kp / 128};
+  cuuint64_t strides[2] = {kp / 8, 16};
+  cuuint32_t box[3] = {16, 128, 2};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? SLSP_OK : SLSP_ERR_CUDA;
+}
+
+int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return sms;
+}
+
+template <typename C>
+int run(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, Params p, cudaStream_t s) {
+  static bool configured = false;
+  auto kern = gemm_kernel<C>;
+  if (!configured) {
+    SLSP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    configured = true;
+  }
+  p.m_tiles = static_cast<int>((p.n + C::BM - 1) / C::BM);
+  p.n_tiles = static_cast<int>((p.m + C::BN - 1) / C::BN);
+  const int tiles = p.m_tiles * p.n_tiles;
+  if (tiles == 0) return SLSP_OK;
+  int clusters = num_sms() / 2;
+  if (clusters > tiles) clusters = tiles;
+  kern<<<2 * clusters, kNumThreads, C::SMEM, s>>>(a, b, e, p);
+  SLSP_LAUNCH_CHECK();
+  return SLSP_OK;
+}
+
+template <bool SPARSE, MmaKind K, int BN, int ST>
+int run_out(int out_mode, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const Params& p,
+            cudaStream_t s) {
+  switch (out_mode) {
+    case SLSP_OUT_RAW_NM: return run<Cfg<SPARSE, K, BN, ST, SLSP_OUT_RAW_NM>>(a, b, e, p, s);
+    case SLSP_OUT_BF16_NM: return run<Cfg<SPARSE, K, BN, ST, SLSP_OUT_BF16_NM>>(a, b, e, p, s);
+    case SLSP_OUT_BF16_MN: return run<Cfg<SPARSE, K, BN, ST, SLSP_OUT_BF16_MN>>(a, b, e, p, s);
+  }
+  return SLSP_ERR_INVALID;
+}
+
+constexpr int kSparseBN = 224;
+constexpr int kSparseStages = 4;
+constexpr int kDenseBN = 256;
+constexpr int kDenseStages = 6;
+
+int check_out(int out_mode, const float* s_ch, const float* s_tok, void* out, int64_t ldo, int64_t n, int64_t m) {
+  if (!out) return SLSP_ERR_INVALID;
+  if (out_mode == SLSP_OUT_RAW_NM || out_mode == SLSP_OUT_BF16_NM) {
+    if (ldo < m) return SLSP_ERR_INVALID;
+  } else if (out_mode == SLSP_OUT_BF16_MN) {
+    if (ldo < n) return SLSP_ERR_INVALID;
+  } else {
+    return SLSP_ERR_INVALID;
+  }
+  if (out_mode != SLSP_OUT_RAW_NM && (!s_ch || !s_tok)) return SLSP_ERR_INVALID;
+  return SLSP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int slsp_sparse_gemm(int dtype, const void* values, const uint8_t* meta, int64_t n, int64_t kp, const void* act,
+                     int64_t m, const float* s_ch, const float* s_tok, int out_mode, void* out, int64_t ldo,
+                     slsp_stream_t stream) {
+  using namespace slsp_host;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (n < 0 || m < 0 || kp <= 0) return SLSP_ERR_INVALID;
+  if (kp % 256 != 0) return SLSP_ERR_DIMENSION;
+  if (kp > (int64_t{1} << 23)) return SLSP_ERR_INVALID;  // gemm.hpp:56 int8 accumulator bound
+  if (n > (int64_t{1} << 31) - 256 || m > (int64_t{1} << 31) - 256) return SLSP_ERR_UNSUPPORTED;
+  int st = check_out(out_mode, s_ch, s_tok, out, ldo, n, m);
+  if (st) return st;
+  if (dtype != SLSP_DT_I8 && dtype != SLSP_DT_E4M3) return SLSP_ERR_UNSUPPORTED;
+  if ((st = require_sm100())) return st;
+  if (n == 0 || m == 0) return SLSP_OK;
+  CUtensorMap ta, tb, te;
+  if ((st = make_map_2d(&ta, values, kp / 2, n, 128))) return st;
+  if ((st = make_map_2d(&tb, act, kp, m, kSparseBN / 2))) return st;
+  if ((st = make_map_meta(&te, meta, n, kp))) return st;
+  Params p{};
+  p.n = n;
+  p.m = m;
+  p.num_kb = static_cast<int>(kp / 256);
+  p.s_ch = s_ch;
+  p.s_tok = s_tok;
+  p.out = out;
+  p.ldo = ldo;
+  if (dtype == SLSP_DT_I8)
+    return run_out<true, MmaKind::I8, kSparseBN, kSparseStages>(out_mode, ta, tb, te, p, s);
+  return run_out<true, MmaKind::F8, kSparseBN, kSparseStages>(out_mode, ta, tb, te, p, s);
+}
+
+int slsp_dense_gemm(int dtype, const void* w, int64_t n, int64_t k, const void* act, int64_t m, const float* s_ch,
+                    const float* s_tok, int out_mode, void* out, int64_t ldo, slsp_stream_t stream) {
+  using namespace slsp_host;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (n < 0 || m < 0 || k <= 0) return SLSP_ERR_INVALID;
+  const int esz = elem_size(dtype);
+  if (dtype != SLSP_DT_I8 && dtype != SLSP_DT_E4M3 && dtype != SLSP_DT_BF16) return SLSP_ERR_UNSUPPORTED;
+  if ((k * esz) % 128 != 0) return SLSP_ERR_DIMENSION;
+  if (dtype == SLSP_DT_I8 && k > (int64_t{1} << 23)) return SLSP_ERR_INVALID;  // gemm.hpp:147-149
+  if (n > (int64_t{1} << 31) - 256 || m > (int64_t{1} << 31) - 256) return SLSP_ERR_UNSUPPORTED;
+  int st = check_out(out_mode, s_ch, s_tok, out, ldo, n, m);
+  if (st) return st;
+  if ((st = require_sm100())) return st;
+  if (n == 0 || m == 0) return SLSP_OK;
+  CUtensorMap ta, tb, te;
+  if ((st = make_map_2d(&ta, w, k * esz, n, 128))) return st;
+  if ((st = make_map_2d(&tb, act, k * esz, m, kDenseBN / 2))) return st;
+  te = ta;
+  Params p{};
+  p.n = n;
+  p.m = m;
+  p.num_kb = static_cast<int>(k * esz / 128);
+  p.s_ch = s_ch;
+  p.s_tok = s_tok;
+  p.out = out;
+  p.ldo = ldo;
+  if (dtype == SLSP_DT_I8) return run_out<false, MmaKind::I8, kDenseBN, kDenseStages>(out_mode, ta, tb, te, p, s);
+  if (dtype == SLSP_DT_E4M3) return run_out<false, MmaKind::F8, kDenseBN, kDenseStages>(out_mode, ta, tb, te, p, s);
+  return run_out<false, MmaKind::F16, kDenseBN, kDenseStages>(out_mode, ta, tb, te, p, s);
+}
+
+}  // extern "C"

@@ -1,0 +1,53 @@
+// Host-side helpers shared by the C-ABI translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/slsp_b200.h"
+
+namespace slsp_host {
+
+// Records the CUDA error text for slsp_last_cuda_error() and returns SLSP_ERR_CUDA.
+int cuda_fail(cudaError_t e, const char* what);
+
+#define SLSP_CUDA_TRY(expr)                                  \
+  do {                                                       \
+    cudaError_t e__ = (expr);                                \
+    if (e__ != cudaSuccess) return ::slsp_host::cuda_fail(e__, #expr); \
+  } while (0)
+
+#define SLSP_LAUNCH_CHECK() SLSP_CUDA_TRY(cudaGetLastError())
+
+// Window plan for hw 2:4 (pattern.hpp:107-154). Returns SLSP_OK or SLSP_ERR_PLAN/INVALID.
+int plan(int z, int l, int* wc);
+
+// Sentinel written into the status scratch before a checking kernel.
+constexpr unsigned long long kNoError = ~0ull;
+
+// Clears the status scratch (async).
+int status_reset(void* status_ws, cudaStream_t s);
+// Synchronises `s`, reads the min-reduced (row << 32 | index) key.
+// Returns SLSP_OK when no error was recorded, else `err_code` with the location.
+int status_collect(void* status_ws, cudaStream_t s, int err_code, int64_t* row, int64_t* index);
+
+// Current device must be sm_100 (B200); fails loudly otherwise.
+int require_sm100();
+
+inline int elem_size(int dtype) {
+  switch (dtype) {
+    case SLSP_DT_I8:
+    case SLSP_DT_E4M3:
+      return 1;
+    case SLSP_DT_BF16:
+      return 2;
+    case SLSP_DT_F32:
+      return 4;
+    case SLSP_DT_F64:
+      return 8;
+    default:
+      return 0;
+  }
+}
+
+}  // namespace slsp_host

@@ -1,0 +1,323 @@
+// Activation Lifting Ψ on sm_100a: per-token absmax + quantization fused with
+// the window-duplicating rearrangement K -> K'.
+//
+// One CTA per token row (grid-stride). Pass 1 streams the row into shared
+// memory with 16-byte coalesced loads while reducing |x| (warp shuffles +
+// one smem hop). Pass 2 quantizes every SOURCE element exactly once in
+// double precision (the reference computes x*r in double, quantize.hpp:151,
+// :163 — fp32 math would flip ~4e-4 of the codes). Pass 3
+// emits the lifted words: word j = window j of group g = j/wc, source offset
+// l*g + 2*(j%wc), written as 16-byte vector stores.
+#include "common.cuh"
+#include "internal.h"
+
+namespace {
+
+using namespace slsp_dev;
+
+constexpr int kThreads = 256;
+
+enum : int { IN_F32 = 0, IN_BF16 = 1 };
+enum : int { K_INT8 = 0, K_FP8 = 1, K_NONE = 2 };
+
+template <int IN>
+SLSP_DEVINL float in_value(const uint8_t* s, int64_t k) {
+  if constexpr (IN == IN_F32) return reinterpret_cast<const float*>(s)[k];
+  return __uint_as_float(static_cast<uint32_t>(reinterpret_cast<const uint16_t*>(s)[k]) << 16);
+}
+
+struct ActArgs {
+  const uint8_t* x;
+  int64_t rows, cols;
+  int l, wc, kind;
+  int64_t in_cols_pad;  // ceil(cols/l)*l: zero-padded source width (quantize.hpp:130,162)
+  int64_t words_real;   // lifted windows per row (LIFT) — unused otherwise
+  int64_t out_bytes;    // bytes written per row (kp or kpad, times element size for K_NONE)
+  uint8_t* out;
+  float* scales;
+  unsigned long long* status;
+};
+
+template <int IN, int KIND, bool LIFT>
+__global__ void __launch_bounds__(kThreads) act_kernel(ActArgs a) {
+  constexpr int ESZ = IN == IN_F32 ? 4 : 2;
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ float s_red[kThreads / 32];
+  __shared__ int s_bad[kThreads / 32];
+  uint8_t* s_x = smem;                                       // raw source row, padded
+  uint8_t* s_q = smem + ((a.in_cols_pad * ESZ + 15) & ~15);  // quantized codes (KIND != NONE)
+  const int warp = threadIdx.x >> 5;
+
+  for (int64_t row = blockIdx.x; row < a.rows; row += gridDim.x) {
+    const uint8_t* src = a.x + row * a.cols * ESZ;
+    // ---- pass 1: row -> smem, |x| max, finiteness ----
+    float amax = 0.f;
+    int bad = 0;
+    const int64_t nbytes = a.cols * ESZ;
+    const bool vec = ((reinterpret_cast<uintptr_t>(src) & 15u) == 0);
+    int64_t done = 0;
+    if (vec) {
+      const int64_t nvec = nbytes >> 4;
+      for (int64_t i = threadIdx.x; i < nvec; i += kThreads) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(src) + i);
+        reinterpret_cast<uint4*>(s_x)[i] = v;
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if constexpr (IN == IN_F32) {
+            const float f = __uint_as_float(w[j]);
+            bad |= !isfinite(f);
+            amax = fmaxf(amax, fabsf(f));
+          } else {
+            const float f0 = __uint_as_float(w[j] << 16), f1 = __uint_as_float(w[j] & 0xFFFF0000u);
+            bad |= !isfinite(f0) | !isfinite(f1);
+            amax = fmaxf(amax, fmaxf(fabsf(f0), fabsf(f1)));
+          }
+        }
+      }
+      done = nvec << 4;
+    }
+    for (int64_t b = done / ESZ + threadIdx.x; b < a.cols; b += kThreads) {
+      const float f = in_value<IN>(src, b);
+      if constexpr (IN == IN_F32) reinterpret_cast<float*>(s_x)[b] = f;
+      else reinterpret_cast<uint16_t*>(s_x)[b] = reinterpret_cast<const uint16_t*>(src)[b];
+      bad |= !isfinite(f);
+      amax = fmaxf(amax, fabsf(f));
+    }
+    for (int64_t b = a.cols + threadIdx.x; b < a.in_cols_pad; b += kThreads) {  // zero pad
+      if constexpr (IN == IN_F32) reinterpret_cast<float*>(s_x)[b] = 0.f;
+      else reinterpret_cast<uint16_t*>(s_x)[b] = 0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+      bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      s_red[warp] = amax;
+      s_bad[warp] = bad;
+    }
+    __syncthreads();
+    amax = 0.f;
+    bad = 0;
+#pragma unroll
+    for (int i = 0; i < kThreads / 32; ++i) {
+      amax = fmaxf(amax, s_red[i]);
+      bad |= s_bad[i];
+    }
+    if (bad && threadIdx.x == 0) atomicMin(a.status, static_cast<unsigned long long>(row) << 32);
+
+    if constexpr (KIND != K_NONE) {
+      // quantize.hpp:151-153: r = qmax/absmax, scale = float(absmax/qmax), in double.
+      const double qmax = KIND == K_INT8 ? 127.0 : 448.0;
+      const double absmax = static_cast<double>(amax);
+      const double r = absmax == 0.0 ? 0.0 : qmax / absmax;
+      if (threadIdx.x == 0) a.scales[row] = absmax == 0.0 ? 1.0f : __double2float_rn(absmax / qmax);
+      // ---- pass 2: quantize each source element once ----
+      for (int64_t k = threadIdx.x; k < a.in_cols_pad; k += kThreads)
+        s_q[k] = quantize_value(static_cast<double>(in_value<IN>(s_x, k)) * r, KIND);
+    }
+    __syncthreads();
+
+    // ---- pass 3: emit the row, 16 bytes per thread per step ----
+    uint8_t* dst = a.out + row * a.out_bytes;
+    const int64_t nchunks = a.out_bytes >> 4;
+    for (int64_t c = threadIdx.x; c < nchunks; c += kThreads) {
+      uint32_t o[4];
+      if constexpr (KIND != K_NONE && LIFT) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int64_t j = c * 4 + i;  // lifted word = window j
+          uint32_t word = 0;
+          if (j < a.words_real) {
+            const int64_t g = j / a.wc;
+            const int64_t b = g * a.l + 2 * (j - g * a.wc);
+            const uint16_t lo = *reinterpret_cast<const uint16_t*>(s_q + b);
+            const uint16_t hi = *reinterpret_cast<const uint16_t*>(s_q + b + 2);
+            word = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+          }
+          o[i] = word;
+        }
+      } else if constexpr (KIND != K_NONE) {  // quantize_rows: identity layout
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          uint32_t word = 0;
+          for (int d = 0; d < 4; ++d) {
+            const int64_t k = c * 16 + i * 4 + d;
+            if (k < a.cols) word |= static_cast<uint32_t>(s_q[k]) << (8 * d);
+          }
+          o[i] = word;
+        }
+      } else {  // BF16/FP32 passthrough lift (lift_row, quantize.hpp:72-89)
+        constexpr int PER = 16 / ESZ;  // elements per 16-byte chunk
+        uint8_t* ob = reinterpret_cast<uint8_t*>(o);
+#pragma unroll
+        for (int e = 0; e < PER; ++e) {
+          const int64_t p = c * PER + e;  // lifted element index
+          const int64_t j = p >> 2;
+          if (j < a.words_real) {
+            const int64_t g = j / a.wc;
+            const int64_t b = g * a.l + 2 * (j - g * a.wc) + (p & 3);
+            if constexpr (ESZ == 2)
+              reinterpret_cast<uint16_t*>(ob)[e] = reinterpret_cast<const uint16_t*>(s_x)[b];
+            else
+              reinterpret_cast<uint32_t*>(ob)[e] = reinterpret_cast<const uint32_t*>(s_x)[b];
+          } else {
+            if constexpr (ESZ == 2) reinterpret_cast<uint16_t*>(ob)[e] = 0;
+            else reinterpret_cast<uint32_t*>(ob)[e] = 0;
+          }
+        }
+      }
+      reinterpret_cast<uint4*>(dst)[c] = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+    __syncthreads();
+  }
+}
+
+template <int IN, int KIND, bool LIFT>
+int launch_act(ActArgs& a, int esz, cudaStream_t s) {
+  if (a.rows == 0) return SLSP_OK;
+  const size_t smem = ((a.in_cols_pad * esz + 15) & ~static_cast<int64_t>(15)) + (KIND != K_NONE ? a.in_cols_pad : 0);
+  if (smem > 200 * 1024) return SLSP_ERR_UNSUPPORTED;
+  auto k = act_kernel<IN, KIND, LIFT>;
+  SLSP_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int per_sm = 1;
+  SLSP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, smem));
+  int dev = 0, sms = 148;
+  SLSP_CUDA_TRY(cudaGetDevice(&dev));
+  SLSP_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int64_t cap = static_cast<int64_t>(sms) * (per_sm > 0 ? per_sm : 1);
+  const unsigned grid = static_cast<unsigned>(a.rows < cap ? a.rows : cap);
+  k<<<grid, kThreads, smem, s>>>(a);
+  SLSP_LAUNCH_CHECK();
+  return SLSP_OK;
+}
+
+template <bool LIFT>
+int dispatch_quant(int in_dtype, int kind, ActArgs& a, cudaStream_t s) {
+  const int esz = in_dtype == SLSP_DT_F32 ? 4 : 2;
+  if (in_dtype == SLSP_DT_F32) {
+    return kind == SLSP_QUANT_INT8 ? launch_act<IN_F32, K_INT8, LIFT>(a, esz, s)
+                                   : launch_act<IN_F32, K_FP8, LIFT>(a, esz, s);
+  }
+  return kind == SLSP_QUANT_INT8 ? launch_act<IN_BF16, K_INT8, LIFT>(a, esz, s)
+                                 : launch_act<IN_BF16, K_FP8, LIFT>(a, esz, s);
+}
+
+// Scratch for the mandatory-in-kernel status word when the caller skips checks.
+struct StatusScope {
+  unsigned long long* ptr = nullptr;
+  unsigned long long* owned = nullptr;
+  cudaStream_t s{};
+  int init(void* ws, cudaStream_t st) {
+    s = st;
+    if (ws) {
+      ptr = static_cast<unsigned long long*>(ws);
+      return slsp_host::status_reset(ws, st);
+    }
+    SLSP_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&owned), sizeof(unsigned long long), st));
+    ptr = owned;
+    return SLSP_OK;
+  }
+  ~StatusScope() {
+    if (owned) cudaFreeAsync(owned, s);
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+int slsp_fused_quant_slide(int in_dtype, const void* x, int64_t rows, int64_t cols, int z, int l, int kind,
+                           int64_t kp, uint32_t* payload, float* scales, void* status_ws, int64_t* bad_row,
+                           slsp_stream_t stream) {
+  using namespace slsp_host;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int wc = 0;
+  int st = plan(z, l, &wc);  // pattern.hpp plan; hw_n == 4 by construction (quantize.hpp:125)
+  if (st) return st;
+  if ((in_dtype != SLSP_DT_F32 && in_dtype != SLSP_DT_BF16) || (kind != 0 && kind != 1)) return SLSP_ERR_INVALID;
+  if (rows < 0 || cols < 0) return SLSP_ERR_INVALID;
+  const int64_t groups = (cols + l - 1) / l;
+  const int64_t words = groups * wc;
+  if (kp < words * 4 || kp % 16 != 0) return SLSP_ERR_DIMENSION;
+  if ((st = require_sm100())) return st;
+  StatusScope ss;
+  if ((st = ss.init(status_ws, s))) return st;
+  ActArgs a{};
+  a.x = static_cast<const uint8_t*>(x);
+  a.rows = rows;
+  a.cols = cols;
+  a.l = l;
+  a.wc = wc;
+  a.kind = kind;
+  a.in_cols_pad = groups * l;
+  a.words_real = words;
+  a.out_bytes = kp;
+  a.out = reinterpret_cast<uint8_t*>(payload);
+  a.scales = scales;
+  a.status = ss.ptr;
+  if ((st = dispatch_quant<true>(in_dtype, kind, a, s))) return st;
+  return status_collect(status_ws, s, SLSP_ERR_NON_FINITE, bad_row, nullptr);
+}
+
+int slsp_quantize_rows(int in_dtype, const void* x, int64_t rows, int64_t cols, int kind, int64_t kpad, uint8_t* out,
+                       float* scales, void* status_ws, int64_t* bad_row, slsp_stream_t stream) {
+  using namespace slsp_host;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if ((in_dtype != SLSP_DT_F32 && in_dtype != SLSP_DT_BF16) || (kind != 0 && kind != 1)) return SLSP_ERR_INVALID;
+  if (rows < 0 || cols < 0) return SLSP_ERR_INVALID;
+  if (kpad < cols || kpad % 16 != 0) return SLSP_ERR_DIMENSION;
+  int st;
+  if ((st = require_sm100())) return st;
+  StatusScope ss;
+  if ((st = ss.init(status_ws, s))) return st;
+  ActArgs a{};
+  a.x = static_cast<const uint8_t*>(x);
+  a.rows = rows;
+  a.cols = cols;
+  a.l = 1;
+  a.wc = 1;
+  a.kind = kind;
+  a.in_cols_pad = cols;
+  a.words_real = 0;
+  a.out_bytes = kpad;
+  a.out = out;
+  a.scales = scales;
+  a.status = ss.ptr;
+  if ((st = dispatch_quant<false>(in_dtype, kind, a, s))) return st;
+  return status_collect(status_ws, s, SLSP_ERR_NON_FINITE, bad_row, nullptr);
+}
+
+int slsp_lift_rows(int dtype, const void* x, int64_t rows, int64_t cols, int z, int l, int64_t kp, void* out,
+                   slsp_stream_t stream) {
+  using namespace slsp_host;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int wc = 0;
+  int st = plan(z, l, &wc);
+  if (st) return st;
+  if (dtype != SLSP_DT_BF16 && dtype != SLSP_DT_F32) return SLSP_ERR_UNSUPPORTED;
+  if (rows < 0 || cols < 0) return SLSP_ERR_INVALID;
+  if (cols % l != 0) return SLSP_ERR_DIMENSION;  // quantize.hpp:78-81
+  const int esz = elem_size(dtype);
+  const int64_t words = cols / l * wc;
+  if (kp < words * 4 || (kp * esz) % 16 != 0) return SLSP_ERR_DIMENSION;
+  if ((st = require_sm100())) return st;
+  StatusScope ss;
+  if ((st = ss.init(nullptr, s))) return st;
+  ActArgs a{};
+  a.x = static_cast<const uint8_t*>(x);
+  a.rows = rows;
+  a.cols = cols;
+  a.l = l;
+  a.wc = wc;
+  a.in_cols_pad = cols;
+  a.words_real = words;
+  a.out_bytes = kp * esz;
+  a.out = static_cast<uint8_t*>(out);
+  a.status = ss.ptr;
+  return dtype == SLSP_DT_BF16 ? launch_act<IN_BF16, K_NONE, true>(a, esz, s)
+                               : launch_act<IN_F32, K_NONE, true>(a, esz, s);
+}
+
+}  // extern "C"

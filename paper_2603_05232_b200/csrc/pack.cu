@@ -1,0 +1,395 @@
+// Offline weight transform Φ on sm_100a: Sliding Window Decomposition packer,
+// compressor and magnitude pruner.
+//
+// Memory-bound integer/byte work: one thread per l-element source block
+// ("group"); the greedy placement depends only on the block's l-bit nonzero
+// mask, so it runs in registers on bit masks. Outputs are staged in shared
+// memory per 256-group chunk and written back with 32-bit coalesced stores.
+#include "common.cuh"
+#include "internal.h"
+
+namespace {
+
+using namespace slsp_dev;
+
+constexpr int kThreads = 256;
+constexpr int kMaxL = 32;
+
+// matrix.hpp:63-67 is_nonzero (v != T{}): -0.0 is zero, NaN is nonzero.
+// e4m3 codes are judged by decoded value: 0x00 and 0x80 are zero.
+template <int ESZ>
+SLSP_DEVINL bool nonzero_bits(uint64_t bits, int dtype) {
+  if constexpr (ESZ == 1) return dtype == SLSP_DT_E4M3 ? (bits & 0x7Fu) != 0 : (bits & 0xFFu) != 0;
+  if constexpr (ESZ == 2) return (bits & 0x7FFFu) != 0;
+  if constexpr (ESZ == 4) return (bits & 0x7FFFFFFFu) != 0;
+  return (bits & 0x7FFFFFFFFFFFFFFFull) != 0;
+}
+
+template <int ESZ>
+SLSP_DEVINL uint64_t load_elem(const uint8_t* base, int64_t idx) {
+  if constexpr (ESZ == 1) return __ldg(base + idx);
+  if constexpr (ESZ == 2) return __ldg(reinterpret_cast<const uint16_t*>(base) + idx);
+  if constexpr (ESZ == 4) return __ldg(reinterpret_cast<const uint32_t*>(base) + idx);
+  return __ldg(reinterpret_cast<const unsigned long long*>(base) + idx);
+}
+
+template <int ESZ>
+SLSP_DEVINL void store_elem(uint8_t* base, int64_t idx, uint64_t v) {
+  if constexpr (ESZ == 1) base[idx] = static_cast<uint8_t>(v);
+  if constexpr (ESZ == 2) reinterpret_cast<uint16_t*>(base)[idx] = static_cast<uint16_t>(v);
+  if constexpr (ESZ == 4) reinterpret_cast<uint32_t*>(base)[idx] = static_cast<uint32_t>(v);
+  if constexpr (ESZ == 8) reinterpret_cast<unsigned long long*>(base)[idx] = v;
+}
+
+SLSP_DEVINL void record_error(unsigned long long* status, int64_t row, int64_t index) {
+  atomicMin(status, (static_cast<unsigned long long>(row) << 32) | static_cast<unsigned long long>(index));
+}
+
+// Block-cooperative copy smem -> global: 32-bit stores when the destination
+// is 4-byte aligned, bytes otherwise.
+SLSP_DEVINL void copy_out(uint8_t* dst, const uint8_t* src, int64_t nbytes) {
+  if ((reinterpret_cast<uintptr_t>(dst) & 3u) == 0) {
+    const int64_t nw = nbytes >> 2;
+    for (int64_t i = threadIdx.x; i < nw; i += blockDim.x)
+      reinterpret_cast<uint32_t*>(dst)[i] = reinterpret_cast<const uint32_t*>(src)[i];
+    for (int64_t i = (nw << 2) + threadIdx.x; i < nbytes; i += blockDim.x) dst[i] = src[i];
+  } else {
+    for (int64_t i = threadIdx.x; i < nbytes; i += blockDim.x) dst[i] = src[i];
+  }
+}
+
+struct PackArgs {
+  const uint8_t* w;
+  int64_t rows, cols;
+  int z, l, wc, dtype;
+  int64_t groups_real;  // ceil(cols / l)
+  int64_t group_slots;  // groups covering the output width
+  int64_t out_windows;  // windows written per row
+  uint8_t* out_a;       // MODE 0: slided; MODE 1: values
+  uint8_t* out_meta;    // MODE 1: packed codes
+  int64_t ld_a_bytes;   // row stride of out_a in bytes
+  int64_t ld_meta;      // row stride of out_meta in bytes
+  unsigned long long* status;
+};
+
+// MODE 0: pack_matrix (pack.hpp:171-204) -> slided rows of wc*4 per group.
+// MODE 1: pack + compress fused (pack.hpp:83-122 + gemm.hpp:70-110) ->
+//         values (2 per window) + packed 2-bit codes (container.hpp:330-336).
+template <int ESZ, int MODE>
+__global__ void __launch_bounds__(kThreads) pack_kernel(PackArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int wc = a.wc;
+  const int64_t chunk = blockIdx.x;
+  const int64_t gs = chunk * kThreads + threadIdx.x;
+  const int64_t win0 = chunk * kThreads * wc;  // first window of this chunk
+  const int64_t chunk_windows = imin64(static_cast<int64_t>(kThreads) * wc, a.out_windows - win0);
+  // MODE 1 staging: values [kThreads*wc*2*ESZ] then meta words; MODE 0: slided.
+  uint8_t* s_vals = smem;
+  uint32_t* s_meta = reinterpret_cast<uint32_t*>(smem + kThreads * wc * 2 * ESZ);
+  const int meta_words = (kThreads * wc + 7) / 8;
+
+  for (int64_t row = blockIdx.y; row < a.rows; row += gridDim.y) {
+    if (MODE == 1)
+      for (int i = threadIdx.x; i < meta_words; i += kThreads) s_meta[i] = 0;
+    __syncthreads();
+    if (gs < a.group_slots) {
+      const uint8_t* src = a.w + (row * a.cols) * ESZ;
+      const int64_t col0 = gs * a.l;
+      uint32_t mask = 0;
+      if (gs < a.groups_real) {
+        for (int k = 0; k < a.l; ++k) {
+          const int64_t col = col0 + k;
+          if (col < a.cols && nonzero_bits<ESZ>(load_elem<ESZ>(src, col), a.dtype)) mask |= 1u << k;
+        }
+      }
+      if (__popc(mask) > a.z) {
+        record_error(a.status, row, gs);  // first_overfull_block, pack.hpp:124-133
+      }
+      // greedy_pack_row (pack.hpp:94-111): windows in order, offsets in order,
+      // accept an unused nonzero while the window holds < 2.
+      uint32_t used = 0;
+      for (int w = 0; w < wc; ++w) {
+        const int s = 2 * w;
+        int p[2] = {-1, -1};
+        int cnt = 0;
+        for (int d = 0; d < 4; ++d) {
+          const int k = s + d;
+          if (((mask >> k) & 1u) && !((used >> k) & 1u) && cnt < 2) {
+            used |= 1u << k;
+            p[cnt++] = d;
+          }
+        }
+        const int64_t wl = static_cast<int64_t>(threadIdx.x) * wc + w;  // window index within chunk
+        if (wl >= chunk_windows) continue;
+        if (MODE == 0) {
+          uint8_t* dst = s_vals + wl * 4 * ESZ;
+          for (int d = 0; d < 4; ++d) {
+            const bool take = (p[0] == d) || (p[1] == d);
+            store_elem<ESZ>(dst, d, take ? load_elem<ESZ>(src, col0 + s + d) : 0ull);
+          }
+        } else {
+          // compress canonical padding (gemm.hpp:99-102): fill with the
+          // smallest unused positions, then sort; padded values are T{}.
+          uint64_t v0 = 0, v1 = 0;
+          int c0, c1;
+          if (cnt == 2) {
+            c0 = p[0];
+            c1 = p[1];
+            v0 = load_elem<ESZ>(src, col0 + s + c0);
+            v1 = load_elem<ESZ>(src, col0 + s + c1);
+          } else if (cnt == 1) {
+            const uint64_t v = load_elem<ESZ>(src, col0 + s + p[0]);
+            if (p[0] == 0) {
+              c0 = 0; c1 = 1; v0 = v;
+            } else {
+              c0 = 0; c1 = p[0]; v1 = v;
+            }
+          } else {
+            c0 = 0;
+            c1 = 1;
+          }
+          store_elem<ESZ>(s_vals, wl * 2, v0);
+          store_elem<ESZ>(s_vals, wl * 2 + 1, v1);
+          const uint32_t nib = static_cast<uint32_t>(c0 | (c1 << 2));
+          atomicOr(&s_meta[wl >> 3], nib << (4 * (wl & 7)));
+        }
+      }
+      if (mask & ~used) record_error(a.status, row, gs);  // leftover, pack.hpp:112-119
+    }
+    __syncthreads();
+    if (chunk_windows > 0) {
+      if (MODE == 0) {
+        copy_out(a.out_a + row * a.ld_a_bytes + win0 * 4 * ESZ, s_vals, chunk_windows * 4 * ESZ);
+      } else {
+        copy_out(a.out_a + row * a.ld_a_bytes + win0 * 2 * ESZ, s_vals, chunk_windows * 2 * ESZ);
+        copy_out(a.out_meta + row * a.ld_meta + win0 / 2, reinterpret_cast<const uint8_t*>(s_meta),
+                 (chunk_windows + 1) / 2);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// gemm.hpp:70-110 compress: one thread per 4-window of a slided row.
+template <int ESZ>
+__global__ void compress_kernel(const uint8_t* slided, int64_t rows, int64_t wpr, int dtype, uint8_t* values,
+                                uint8_t* codes, unsigned long long* status) {
+  const int64_t total = rows * wpr;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    uint64_t v[4];
+    int pos[4], np = 0;
+    for (int d = 0; d < 4; ++d) {
+      v[d] = load_elem<ESZ>(slided, i * 4 + d);
+      if (nonzero_bits<ESZ>(v[d], dtype)) pos[np++] = d;
+    }
+    if (np > 2) {
+      record_error(status, i / wpr, i % wpr);
+      continue;
+    }
+    for (int d = 0; np < 2; ++d) {
+      bool found = false;
+      for (int j = 0; j < np; ++j) found |= pos[j] == d;
+      if (!found) pos[np++] = d;
+    }
+    if (pos[0] > pos[1]) {
+      const int t = pos[0];
+      pos[0] = pos[1];
+      pos[1] = t;
+    }
+    store_elem<ESZ>(values, i * 2, v[pos[0]]);
+    store_elem<ESZ>(values, i * 2 + 1, v[pos[1]]);
+    codes[i * 2] = static_cast<uint8_t>(pos[0]);
+    codes[i * 2 + 1] = static_cast<uint8_t>(pos[1]);
+  }
+}
+
+// pack.hpp:238-261 magnitude_prune: zero the l-z smallest |v| per block,
+// ties pruned lower-index first (stable_sort order). One thread per block.
+template <int ESZ>
+SLSP_DEVINL double magnitude(uint64_t bits, int dtype) {
+  if constexpr (ESZ == 1) {
+    if (dtype == SLSP_DT_E4M3) return fabs(static_cast<double>(fp8_e4m3_decode(static_cast<uint8_t>(bits))));
+    return fabs(static_cast<double>(static_cast<int8_t>(bits)));
+  }
+  if constexpr (ESZ == 2) return fabs(static_cast<double>(__uint_as_float(static_cast<uint32_t>(bits) << 16)));
+  if constexpr (ESZ == 4) return fabs(static_cast<double>(__uint_as_float(static_cast<uint32_t>(bits))));
+  return fabs(__longlong_as_double(static_cast<long long>(bits)));
+}
+
+template <int ESZ>
+__global__ void prune_kernel(const uint8_t* w, int64_t rows, int64_t cols, int z, int l, int dtype, uint8_t* out) {
+  const int64_t groups = cols / l;
+  const int64_t total = rows * groups;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t base = i * l;  // rows are contiguous blocks of cols = groups*l
+    double mag[kMaxL];
+    for (int k = 0; k < l; ++k) mag[k] = magnitude<ESZ>(load_elem<ESZ>(w, base + k), dtype);
+    const int prune = l - z;
+    for (int k = 0; k < l; ++k) {
+      int rank = 0;
+      for (int j = 0; j < l; ++j) rank += (mag[j] < mag[k]) || (mag[j] == mag[k] && j < k);
+      store_elem<ESZ>(out, base + k, rank < prune ? 0ull : load_elem<ESZ>(w, base + k));
+    }
+  }
+}
+
+template <int MODE>
+int launch_pack(int esz, PackArgs& a, cudaStream_t s) {
+  const int64_t chunks = (a.group_slots + kThreads - 1) / kThreads;
+  if (chunks == 0 || a.rows == 0) return SLSP_OK;
+  size_t smem = MODE == 0 ? static_cast<size_t>(kThreads) * a.wc * 4 * esz
+                          : static_cast<size_t>(kThreads) * a.wc * 2 * esz + ((kThreads * a.wc + 7) / 8) * 4;
+  dim3 grid(static_cast<unsigned>(chunks), static_cast<unsigned>(a.rows < 65535 ? a.rows : 65535));
+  if (chunks > 0x7fffffff) return SLSP_ERR_UNSUPPORTED;
+#define SLSP_PACK_LAUNCH(E)                                                                  \
+  do {                                                                                       \
+    auto k = pack_kernel<E, MODE>;                                                           \
+    if (smem > 48 * 1024)                                                                    \
+      SLSP_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    k<<<grid, kThreads, smem, s>>>(a);                                                       \
+  } while (0)
+  switch (esz) {
+    case 1: SLSP_PACK_LAUNCH(1); break;
+    case 2: SLSP_PACK_LAUNCH(2); break;
+    case 4: SLSP_PACK_LAUNCH(4); break;
+    case 8: SLSP_PACK_LAUNCH(8); break;
+    default: return SLSP_ERR_INVALID;
+  }
+#undef SLSP_PACK_LAUNCH
+  SLSP_LAUNCH_CHECK();
+  return SLSP_OK;
+}
+
+unsigned grid_for(int64_t n, int threads) {
+  int64_t b = (n + threads - 1) / threads;
+  if (b > 148 * 64) b = 148 * 64;
+  return static_cast<unsigned>(b < 1 ? 1 : b);
+}
+
+}  // namespace
+
+extern "C" {
+
+int slsp_pack_matrix(int dtype, const void* w, int64_t rows, int64_t cols, int z, int l, void* slided,
+                     void* status_ws, int64_t* err_row, int64_t* err_block, slsp_stream_t stream) {
+  using namespace slsp_host;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int wc = 0;
+  int st = plan(z, l, &wc);
+  if (st) return st;
+  const int esz = elem_size(dtype);
+  if (!esz || l > kMaxL || rows < 0 || cols < 0) return SLSP_ERR_INVALID;
+  if (cols % l != 0) return SLSP_ERR_DIMENSION;  // pack.hpp:174-177
+  if (!status_ws) return SLSP_ERR_INVALID;       // pack_matrix always reports violations
+  if ((st = require_sm100())) return st;
+  if ((st = status_reset(status_ws, s))) return st;
+  PackArgs a{};
+  a.w = static_cast<const uint8_t*>(w);
+  a.rows = rows;
+  a.cols = cols;
+  a.z = z;
+  a.l = l;
+  a.wc = wc;
+  a.dtype = dtype;
+  a.groups_real = cols / l;
+  a.group_slots = a.groups_real;
+  a.out_windows = a.groups_real * wc;
+  a.out_a = static_cast<uint8_t*>(slided);
+  a.ld_a_bytes = a.out_windows * 4 * esz;
+  a.status = static_cast<unsigned long long*>(status_ws);
+  if ((st = launch_pack<0>(esz, a, s))) return st;
+  return status_collect(status_ws, s, SLSP_ERR_NOT_COMPLIANT, err_row, err_block);
+}
+
+int slsp_pack_compress(int dtype, const void* w, int64_t rows, int64_t cols, int z, int l, int64_t kp, void* values,
+                       uint8_t* meta, void* status_ws, int64_t* err_row, int64_t* err_block, slsp_stream_t stream) {
+  using namespace slsp_host;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int wc = 0;
+  int st = plan(z, l, &wc);
+  if (st) return st;
+  const int esz = elem_size(dtype);
+  if (!esz || esz > 2 || l > kMaxL || rows < 0 || cols < 0) return SLSP_ERR_INVALID;
+  const int64_t groups = (cols + l - 1) / l;
+  const int64_t kprime = groups * wc * 4;
+  if (kp < kprime || kp % 8 != 0) return SLSP_ERR_DIMENSION;
+  if ((st = require_sm100())) return st;
+  if ((st = status_reset(status_ws, s))) return st;
+  unsigned long long* status = static_cast<unsigned long long*>(status_ws);
+  unsigned long long* scratch = nullptr;
+  if (!status) {  // the kernel always reports; park reports in a throwaway word
+    SLSP_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&scratch), sizeof(unsigned long long), s));
+    status = scratch;
+  }
+  PackArgs a{};
+  a.w = static_cast<const uint8_t*>(w);
+  a.rows = rows;
+  a.cols = cols;
+  a.z = z;
+  a.l = l;
+  a.wc = wc;
+  a.dtype = dtype;
+  a.groups_real = groups;
+  a.out_windows = kp / 4;
+  a.group_slots = (a.out_windows + wc - 1) / wc;
+  a.out_a = static_cast<uint8_t*>(values);
+  a.out_meta = meta;
+  a.ld_a_bytes = kp / 2 * esz;
+  a.ld_meta = kp / 8;
+  a.status = status;
+  st = launch_pack<1>(esz, a, s);
+  if (scratch) SLSP_CUDA_TRY(cudaFreeAsync(scratch, s));
+  if (st) return st;
+  return status_collect(status_ws, s, SLSP_ERR_NOT_COMPLIANT, err_row, err_block);
+}
+
+int slsp_compress(int dtype, const void* slided, int64_t rows, int64_t cols_exp, void* values, uint8_t* codes,
+                  void* status_ws, int64_t* err_row, int64_t* err_window, slsp_stream_t stream) {
+  using namespace slsp_host;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int esz = elem_size(dtype);
+  if (!esz || rows < 0 || cols_exp < 0 || !status_ws) return SLSP_ERR_INVALID;
+  if (cols_exp % 4 != 0) return SLSP_ERR_DIMENSION;  // gemm.hpp:78-80
+  int st;
+  if ((st = require_sm100())) return st;
+  if ((st = status_reset(status_ws, s))) return st;
+  const int64_t wpr = cols_exp / 4;
+  const unsigned grid = grid_for(rows * wpr, 256);
+  auto* status = static_cast<unsigned long long*>(status_ws);
+  const auto* in = static_cast<const uint8_t*>(slided);
+  auto* out = static_cast<uint8_t*>(values);
+  switch (esz) {
+    case 1: compress_kernel<1><<<grid, 256, 0, s>>>(in, rows, wpr, dtype, out, codes, status); break;
+    case 2: compress_kernel<2><<<grid, 256, 0, s>>>(in, rows, wpr, dtype, out, codes, status); break;
+    case 4: compress_kernel<4><<<grid, 256, 0, s>>>(in, rows, wpr, dtype, out, codes, status); break;
+    case 8: compress_kernel<8><<<grid, 256, 0, s>>>(in, rows, wpr, dtype, out, codes, status); break;
+  }
+  SLSP_LAUNCH_CHECK();
+  return status_collect(status_ws, s, SLSP_ERR_NOT_COMPLIANT, err_row, err_window);
+}
+
+int slsp_magnitude_prune(int dtype, const void* w, int64_t rows, int64_t cols, int z, int l, void* out,
+                         slsp_stream_t stream) {
+  using namespace slsp_host;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int esz = elem_size(dtype);
+  if (!esz || z <= 0 || l <= 0 || z > l || l > kMaxL || rows < 0 || cols < 0) return SLSP_ERR_INVALID;
+  if (cols % l != 0) return SLSP_ERR_DIMENSION;  // pack.hpp:240-243
+  int st;
+  if ((st = require_sm100())) return st;
+  const unsigned grid = grid_for(rows * (cols / l), 256);
+  const auto* in = static_cast<const uint8_t*>(w);
+  auto* o = static_cast<uint8_t*>(out);
+  switch (esz) {
+    case 1: prune_kernel<1><<<grid, 256, 0, s>>>(in, rows, cols, z, l, dtype, o); break;
+    case 2: prune_kernel<2><<<grid, 256, 0, s>>>(in, rows, cols, z, l, dtype, o); break;
+    case 4: prune_kernel<4><<<grid, 256, 0, s>>>(in, rows, cols, z, l, dtype, o); break;
+    case 8: prune_kernel<8><<<grid, 256, 0, s>>>(in, rows, cols, z, l, dtype, o); break;
+  }
+  SLSP_LAUNCH_CHECK();
+  return SLSP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,95 @@
+// C-ABI plumbing: versioning, status scratch, plan geometry, device checks.
+#include <cstdio>
+#include <cstring>
+
+#include "internal.h"
+
+namespace slsp_host {
+
+static thread_local char g_last_cuda_error[256] = "";
+
+int cuda_fail(cudaError_t e, const char* what) {
+  std::snprintf(g_last_cuda_error, sizeof(g_last_cuda_error), "%s: %s", what, cudaGetErrorString(e));
+  return SLSP_ERR_CUDA;
+}
+
+int plan(int z, int l, int* wc) {
+  int starts[64];
+  return slsp_plan_decomposition(z, l, 2, 4, wc, starts, 64);
+}
+
+int status_reset(void* status_ws, cudaStream_t s) {
+  if (!status_ws) return SLSP_OK;
+  SLSP_CUDA_TRY(cudaMemsetAsync(status_ws, 0xFF, SLSP_STATUS_WS_BYTES, s));
+  return SLSP_OK;
+}
+
+int status_collect(void* status_ws, cudaStream_t s, int err_code, int64_t* row, int64_t* index) {
+  if (!status_ws) return SLSP_OK;
+  unsigned long long key = kNoError;
+  SLSP_CUDA_TRY(cudaMemcpyAsync(&key, status_ws, sizeof(key), cudaMemcpyDeviceToHost, s));
+  SLSP_CUDA_TRY(cudaStreamSynchronize(s));
+  if (key == kNoError) return SLSP_OK;
+  if (row) *row = static_cast<int64_t>(key >> 32);
+  if (index) *index = static_cast<int64_t>(key & 0xFFFFFFFFull);
+  return err_code;
+}
+
+int require_sm100() {
+  int dev = 0;
+  SLSP_CUDA_TRY(cudaGetDevice(&dev));
+  if (!slsp_device_supported(dev)) {
+    std::snprintf(g_last_cuda_error, sizeof(g_last_cuda_error),
+                  "device %d is not an sm_100 (B200) GPU; the slsp_b200 kernels are sm_100a-only", dev);
+    return SLSP_ERR_CUDA;
+  }
+  return SLSP_OK;
+}
+
+}  // namespace slsp_host
+
+extern "C" {
+
+int slsp_version(void) { return 100; }
+
+const char* slsp_status_string(int status) {
+  switch (status) {
+    case SLSP_OK: return "ok";
+    case SLSP_ERR_NOT_COMPLIANT: return "not compliant";
+    case SLSP_ERR_DIMENSION: return "dimension mismatch";
+    case SLSP_ERR_PLAN: return "invalid decomposition plan";
+    case SLSP_ERR_NON_FINITE: return "non-finite input";
+    case SLSP_ERR_INVALID: return "invalid argument";
+    case SLSP_ERR_MALFORMED: return "malformed metadata";
+    case SLSP_ERR_UNSUPPORTED: return "unsupported shape or type";
+    case SLSP_ERR_CUDA: return "CUDA error";
+    default: return "unknown status";
+  }
+}
+
+const char* slsp_last_cuda_error(void) { return slsp_host::g_last_cuda_error; }
+
+int slsp_device_supported(int dev) {
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) return 0;
+  return prop.major == 10 && prop.minor == 0;
+}
+
+// pattern.hpp:107-117 plan_status, pattern.hpp:131-154 plan_decomposition.
+// density < hw_density is decided exactly by cross-multiplication.
+int slsp_plan_decomposition(int z, int l, int hw_m, int hw_n, int* window_count, int* window_starts, int cap) {
+  if (z <= 0 || l <= 0 || z > l || hw_m <= 0 || hw_m >= hw_n) return SLSP_ERR_INVALID;
+  if (static_cast<int64_t>(z) * hw_n < static_cast<int64_t>(hw_m) * l) return SLSP_ERR_PLAN;
+  const int stride = hw_n - hw_m;
+  if (l < hw_n || (l - hw_n) % stride != 0) return SLSP_ERR_PLAN;
+  const int wc = (l - hw_n) / stride + 1;
+  if (static_cast<int64_t>(wc) * hw_m < z) return SLSP_ERR_PLAN;
+  if (window_count) *window_count = wc;
+  if (window_starts) {
+    if (wc > cap) return SLSP_ERR_INVALID;
+    for (int j = 0; j < wc; ++j) window_starts[j] = j * stride;
+  }
+  return SLSP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,152 @@
+"""GPU parity: tcgen05 sparse / dense GEMMs through the C ABI.
+
+INT8: bit-exact int32 accumulators vs the oracle's packed-word sparse_gemm
+(gemm.hpp:199-233) and dense_gemm (gemm.hpp:142-162). BF16 dequant epilogue:
+bit-exact vs the oracle's fp32 restatement (same operation order). FP8:
+relative tolerance vs the double-precision oracle (stated per test)."""
+import numpy as np
+import pytest
+import torch
+
+from helpers import compliant_matrix, lifted_width, mma_format, pad_cols, random_pruned_int8, round_up
+from oracle_lib import DT_E4M3, DT_F32, DT_I8, KIND_FP8, KIND_INT8
+
+pytestmark = pytest.mark.gpu
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def sparse_case(orc, rng, n, k, m, z=6, l=8, exact=False):
+    w = compliant_matrix(rng, n, k // l, z, l, exact_z=exact)
+    x = rng.uniform(-1, 1, size=(m, k)).astype(np.float32)
+    vals, codes = orc.compress(orc.pack_matrix(w, z, l, DT_I8), DT_I8)
+    payload, scales = orc.fused_quant_slide(x, z, l, KIND_INT8, DT_F32)
+    kp = round_up(lifted_width(k, z, l), 256)
+    return w, x, vals, codes, payload, scales, kp
+
+
+def run_sparse_raw(slsp, vals, codes, payload, kp, n, z=6, l=8):
+    v, meta = mma_format(vals, codes, kp)
+    pw = slsp.PackedWeights(dev(v), dev(meta), n, 0, kp, z, l)
+    act = dev(pad_cols(payload.view(np.uint8).reshape(payload.shape[0], -1), kp))
+    return slsp.sparse_gemm(pw, act).cpu().numpy()
+
+
+@pytest.mark.parametrize("n,k,m", [(256, 256, 224), (512, 1024, 448), (300, 400, 250), (1024, 2048, 700)])
+def test_sparse_int8_bit_exact(slsp, orc, n, k, m):
+    rng = np.random.default_rng(n + k + m)
+    w, x, vals, codes, payload, scales, kp = sparse_case(orc, rng, n, k, m)
+    got = run_sparse_raw(slsp, vals, codes, payload, kp, n)
+    want = orc.sparse_gemm_words(vals, codes, payload)
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("z,l", [(4, 6), (8, 10), (14, 16)])
+def test_sparse_int8_other_patterns(slsp, orc, z, l):
+    rng = np.random.default_rng(l)
+    n, m = 256, 224
+    k = l * 40
+    w, x, vals, codes, payload, scales, kp = sparse_case(orc, rng, n, k, m, z, l)
+    got = run_sparse_raw(slsp, vals, codes, payload, kp, n, z, l)
+    assert np.array_equal(got, orc.sparse_gemm_words(vals, codes, payload))
+
+
+def test_sparse_equals_dense_on_quantized(slsp, orc):
+    """test_gemm.cpp:299-323: the packed-word sparse path equals dense_gemm on
+    per-row-quantized X, exactly — here both sides on the GPU kernels."""
+    rng = np.random.default_rng(5)
+    n, k, m = 512, 1024, 448
+    w = random_pruned_int8(rng, n, k, 6, 8)
+    x = torch.from_numpy(rng.uniform(-2, 2, size=(m, k)).astype(np.float32)).cuda()
+    pw = slsp.pack_compress(dev(w), 6, 8)
+    payload, s_tok = slsp.fused_quant_slide(x, 6, 8)
+    ys = slsp.sparse_gemm(pw, payload)
+    q, s2 = slsp.quantize_rows(x)
+    yd = slsp.dense_gemm(dev(w), q.view(torch.int8))
+    assert torch.equal(s_tok, s2)
+    assert torch.equal(ys, yd)
+    want = orc.dense_gemm_i8(w, q.view(torch.int8).cpu().numpy().T.copy())
+    assert np.array_equal(yd.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("n,k,m", [(256, 128, 256), (512, 1024, 512), (300, 384, 260)])
+def test_dense_int8_bit_exact(slsp, orc, n, k, m):
+    rng = np.random.default_rng(n * 3 + k + m)
+    w = rng.integers(-127, 128, size=(n, k)).astype(np.int8)
+    x = rng.integers(-127, 128, size=(m, k)).astype(np.int8)
+    got = slsp.dense_gemm(dev(w), dev(x)).cpu().numpy()
+    assert np.array_equal(got, orc.dense_gemm_i8(w, x.T.copy()))
+
+
+@pytest.mark.parametrize("mode", ["nm", "mn"])
+def test_sparse_bf16_dequant_epilogue(slsp, orc, mode):
+    rng = np.random.default_rng(17)
+    n, k, m = 512, 1024, 300
+    w, x, vals, codes, payload, scales, kp = sparse_case(orc, rng, n, k, m)
+    s_ch = rng.uniform(0.001, 0.02, size=n).astype(np.float32)
+    v, meta = mma_format(vals, codes, kp)
+    pw = slsp.PackedWeights(dev(v), dev(meta), n, k, kp, 6, 8)
+    act = dev(pad_cols(payload.view(np.uint8).reshape(m, -1), kp))
+    out_mode = slsp.OUT_BF16_NM if mode == "nm" else slsp.OUT_BF16_MN
+    y = slsp.sparse_gemm(pw, act, s_ch=dev(s_ch), s_tok=dev(scales), out_mode=out_mode)
+    acc = orc.sparse_gemm_words(vals, codes, payload)
+    want = orc.dequant_bf16(acc, s_ch, scales)
+    got = y.view(torch.int16).cpu().numpy().view(np.uint16)
+    if mode == "mn":
+        got = got.T
+    assert np.array_equal(got, want)
+
+
+def test_sparse_fp8_within_tolerance(slsp, orc):
+    """FP8 e4m3 weights and activations, fp32 accumulation in TMEM vs the
+    double oracle on decoded values. Stated tolerance: |err| <= 2^-14 * sum|w*x|
+    per output (products of e4m3 values are exact in fp32; the bound covers the
+    tensor core's fp32 accumulation order over K'/2 = 768 products)."""
+    rng = np.random.default_rng(23)
+    n, k, m = 512, 1024, 448
+    mask = compliant_matrix(rng, n, k // 8, 6, 8) != 0
+    wf = np.where(mask, rng.uniform(-1, 1, size=mask.shape), 0.0)
+    wcode = np.array([orc.fp8_encode(v) for v in (wf * 200).ravel()], np.uint8).reshape(n, k)
+    wcode[wcode == 0x80] = 0
+    x = rng.uniform(-1, 1, size=(m, k)).astype(np.float32)
+    payload, scales = orc.fused_quant_slide(x, 6, 8, KIND_FP8, DT_F32)
+    vals, codes = orc.compress(orc.pack_matrix(wcode, 6, 8, DT_E4M3), DT_E4M3)
+    kp = round_up(lifted_width(k, 6, 8), 256)
+    v, meta = mma_format(vals, codes, kp)
+    pw = slsp.PackedWeights(dev(v).view(torch.float8_e4m3fn), dev(meta), n, k, kp, 6, 8)
+    act = dev(pad_cols(payload.view(np.uint8).reshape(m, -1), kp))
+    got = slsp.sparse_gemm(pw, act).cpu().numpy().astype(np.float64)
+    dec = np.vectorize(orc.fp8_decode, otypes=[np.float64])
+    vd = dec(vals)
+    ad = dec(payload.view(np.uint8).reshape(m, -1))
+    want = orc.sparse_gemm_f64(vd, codes, ad)
+    absum = orc.sparse_gemm_f64(np.abs(vd), codes, np.abs(ad))
+    rel = np.abs(got - want) / np.maximum(absum, 1e-30)
+    print(f"fp8 max relative error {rel.max():.3e}")
+    assert np.all(np.abs(got - want) <= 2.0 ** -14 * absum + 1e-30)
+
+
+def test_gemm_rejects_bad_kp(slsp):
+    pw = slsp.PackedWeights(torch.zeros(256, 100, dtype=torch.int8, device="cuda"),
+                            torch.zeros(256, 25, dtype=torch.uint8, device="cuda"), 256, 0, 200, 6, 8)
+    with pytest.raises(slsp.DimensionMismatchError):
+        slsp.sparse_gemm(pw, torch.zeros(224, 200, dtype=torch.uint8, device="cuda"))
+
+
+def test_full_shape_sparse_equals_dense(slsp):
+    """Qwen2.5-7B o_proj at M=8192 (full size): sparse(lifted) == dense(quantized)
+    elementwise, exactly (size-independent equivalence, gemm.hpp:258-286)."""
+    g = torch.Generator(device="cuda").manual_seed(1)
+    n = k = 3584
+    m = 8192
+    w = torch.randint(-127, 128, (n, k), dtype=torch.int8, device="cuda", generator=g)
+    w = slsp.magnitude_prune(w, 6, 8)
+    x = (torch.rand(m, k, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    pw = slsp.pack_compress(w, 6, 8)
+    payload, s_tok = slsp.fused_quant_slide(x, 6, 8)
+    q, _ = slsp.quantize_rows(x)
+    ys = slsp.sparse_gemm(pw, payload)
+    yd = slsp.dense_gemm(w, q.view(torch.int8))
+    assert torch.equal(ys, yd)
