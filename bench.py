@@ -1,0 +1,505 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 SlideSparse hot path (BASELINE.json `metric`).
+
+Workload (BASELINE.json configs[1]): every linear layer of Qwen2.5-7B
+(qkv 4608x3584, o 3584x3584, gate_up 37888x3584, down 3584x18944) with 6:8
+INT8 weights at M=8192 tokens. One STEP = for each layer: fused per-token
+quant + activation lifting of that layer's input (slsp_fused_quant_slide)
+then the tcgen05.mma.sp GEMM with the per-token x per-channel dequant
+epilogue to BF16 (slsp_sparse_gemm). The same-precision dense baseline step
+(slsp_quantize_rows + slsp_dense_gemm, also our own sm_100a kernels) is timed
+interleaved in the same process. value = effective TFLOPS = sum(2*M*N*K)/t.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Multi-GPU (torchrun): the output-feature dim N of every layer is sharded
+across ranks (strong scaling, no collective on the GEMM); the optional
+all-gather of the output shards is timed separately. Timing: CUDA events on
+the launching stream, L2 flushed (512 MiB write) between timed steps,
+max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "6:8 sparse GEMM effective TFLOPS & speedup vs dense (M=8192, Qwen2.5-7B shapes)"
+UNIT = "TFLOPS"
+WORKLOADS = {
+    "qwen2.5-7b": [("qkv", 4608, 3584), ("o", 3584, 3584), ("gate_up", 37888, 3584), ("down", 3584, 18944)],
+    "qwen2.5-14b": [("qkv", 7168, 5120), ("o", 5120, 5120), ("gate_up", 27648, 5120), ("down", 5120, 13824)],
+    "llama3.1-8b": [("qkv", 6144, 4096), ("o", 4096, 4096), ("gate_up", 28672, 4096), ("down", 4096, 14336)],
+}
+PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
+TRAFFIC_FILE = ROOT / "profiles" / "traffic.json"
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="qwen2.5-7b")
+    ap.add_argument("--m", type=int, default=8192)
+    ap.add_argument("--pattern", default="6:8")
+    ap.add_argument("--out-mode", choices=["nm", "mn"], default="nm")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--cpu-rows", type=int, default=64, help="weight rows per layer in the CPU sample")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def shard_rows(n: int, world: int, rank: int, align: int = 128) -> tuple[int, int]:
+    per = -(-n // world)
+    per = -(-per // align) * align
+    lo = min(n, rank * per)
+    hi = min(n, lo + per)
+    return lo, hi
+
+
+# ------------------------------------------------------------------ clocks --
+class ClockSampler:
+    """Samples SM clock + throttle reasons through NVML while the timed region runs."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001
+            self.nvml = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nvml.nvmlDeviceGetClockInfo(self.h, self.nvml.NVML_CLOCK_SM))
+                mask = self.nvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.nvml:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nvml:
+            self.t.join()
+
+    def result(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons)}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------- the path --
+class Layer:
+    def __init__(self, slsp, torch, name, n_total, k, lo, hi, m, z, l, gen, device, dense: bool):
+        self.name, self.n_total, self.k, self.lo, self.hi, self.m = name, n_total, k, lo, hi, m
+        self.n = hi - lo
+        self.z, self.l = z, l
+        w = torch.randint(-127, 128, (self.n, k), dtype=torch.int8, device=device, generator=gen)
+        self.w = slsp.magnitude_prune(w, z, l)  # synthetic 6:8 weights (pack.hpp:238-261)
+        del w
+        self.packed = slsp.pack_compress(self.w, z, l)  # offline Φ
+        self.kp = self.packed.kp
+        self.s_ch = (torch.rand(self.n, device=device, generator=gen) * 0.01 + 0.001).float()
+        self.payload = torch.empty((m, self.kp // 4), dtype=torch.int32, device=device)
+        self.s_tok = torch.empty(m, dtype=torch.float32, device=device)
+        self.kpad = -(-k // 128) * 128
+        self.q = torch.empty((m, self.kpad), dtype=torch.uint8, device=device) if dense else None
+        self.q_s = torch.empty(m, dtype=torch.float32, device=device) if dense else None
+        if not dense:
+            self.w = None
+
+    @property
+    def flops(self):
+        return 2.0 * self.m * self.n * self.k
+
+
+def run_b200(args, world, rank, local):
+    import torch
+
+    import paper_2603_05232_b200 as slsp
+
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=device)
+    z, l = (int(v) for v in args.pattern.split(":"))
+    m = args.m
+    gen = torch.Generator(device=device).manual_seed(1234 + rank)
+    out_mode = slsp.OUT_BF16_NM if args.out_mode == "nm" else slsp.OUT_BF16_MN
+
+    layers = []
+    for name, n_total, k in WORKLOADS[args.workload]:
+        lo, hi = shard_rows(n_total, world, rank)
+        layers.append(Layer(slsp, torch, name, n_total, k, lo, hi, m, z, l, gen, device, not args.no_dense))
+    xgen = torch.Generator(device=device).manual_seed(99)  # activations replicated on every rank
+    xs = {k: (torch.rand((m, k), device=device, generator=xgen) * 2 - 1).to(torch.bfloat16)
+          for k in sorted({L.k for L in layers})}
+    outs = [torch.empty((L.n, m) if out_mode == slsp.OUT_BF16_NM else (m, L.n), dtype=torch.bfloat16,
+                        device=device) for L in layers]
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=device)
+
+    # Each kernel call of the step is captured into a CUDA graph, so the timed
+    # region measures device time, not Python launch latency.
+    def op_lift(L):
+        return lambda: slsp.fused_quant_slide(xs[L.k], z, l, kp=L.kp, check=False, payload=L.payload,
+                                              scales=L.s_tok)
+
+    def op_sgemm(L, i):
+        return lambda: slsp.sparse_gemm(L.packed, L.payload, s_ch=L.s_ch, s_tok=L.s_tok, out_mode=out_mode,
+                                        out=outs[i])
+
+    def op_quant(L):
+        return lambda: slsp.quantize_rows(xs[L.k], kpad=L.kpad, check=False, out=L.q, scales=L.q_s)
+
+    def op_dgemm(L, i):
+        return lambda: slsp.dense_gemm(L.w, L.q.view(torch.int8), s_ch=L.s_ch, s_tok=L.q_s, out_mode=out_mode,
+                                       out=outs[i])
+
+    sparse_ops = [f for i, L in enumerate(layers) for f in (op_lift(L), op_sgemm(L, i))]
+    dense_ops = [] if args.no_dense else [f for i, L in enumerate(layers) for f in (op_quant(L), op_dgemm(L, i))]
+    for f in sparse_ops + dense_ops:  # first calls configure kernels outside capture
+        f()
+    torch.cuda.synchronize()
+
+    def capture(fns):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for f in fns:
+                f()
+        return g
+
+    sparse_graph = capture(sparse_ops)
+    dense_graph = capture(dense_ops) if dense_ops else None
+    sparse_op_graphs = [capture([f]) for f in sparse_ops]
+    dense_op_graphs = [capture([f]) for f in dense_ops]
+    stream = torch.cuda.current_stream(device)
+
+    def timed(graph):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        flush.zero_()
+        e0.record(stream)
+        graph.replay()
+        e1.record(stream)
+        return e0, e1
+
+    for _ in range(args.warmup):
+        timed(sparse_graph)
+        if dense_graph:
+            timed(dense_graph)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+
+    sp_events, de_events = [], []
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            sp_events.append(timed(sparse_graph))
+            if dense_graph:
+                de_events.append(timed(dense_graph))
+        torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    sp_ms = sum(a.elapsed_time(b) for a, b in sp_events) / len(sp_events)
+    de_ms = sum(a.elapsed_time(b) for a, b in de_events) / len(de_events) if de_events else None
+
+    # Per-kernel breakdown (separate pass, each kernel alone after an L2 flush).
+    def per_op(graphs, reps=max(3, min(args.steps, 10))):
+        acc = [0.0] * len(graphs)
+        for _ in range(reps):
+            evs = [timed(g) for g in graphs]
+            torch.cuda.synchronize()
+            for j, (a, b) in enumerate(evs):
+                acc[j] += a.elapsed_time(b) / reps
+        return acc[0::2], acc[1::2]
+
+    sp_lift, sp_gemm = per_op(sparse_op_graphs)
+    de_lift, de_gemm = per_op(dense_op_graphs) if dense_op_graphs else (None, None)
+
+    def reduce_max(v):
+        if world == 1 or v is None:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=device)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    sp_ms_max = reduce_max(sp_ms)
+    de_ms_max = reduce_max(de_ms)
+    total_flops = sum(2.0 * m * n * k for _, n, k in WORKLOADS[args.workload])  # whole job, all ranks
+    value = total_flops / (sp_ms_max * 1e-3) / 1e12
+    dense_value = total_flops / (de_ms_max * 1e-3) / 1e12 if de_ms_max else None
+
+    # ---- optional all-gather of the N-sharded outputs (timed separately) ----
+    allgather = None
+    if world > 1:
+        import torch.distributed as dist
+
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        gathered = [torch.empty((m, -(-L.n_total // 128) * 128), dtype=torch.bfloat16, device=device)
+                    for L in layers]
+        if out_mode == slsp.OUT_BF16_MN:
+            for _ in range(2):
+                ev0.record(stream)
+                for i, L in enumerate(layers):
+                    shards = list(gathered[i].view(m, world, -1).unbind(1))
+                    dist.all_gather([s.contiguous() for s in shards], outs[i].contiguous())
+                ev1.record(stream)
+            torch.cuda.synchronize()
+            allgather = {"ms_per_step": reduce_max(ev0.elapsed_time(ev1)),
+                         "bytes_per_rank": sum(2 * m * L.n_total for L in layers)}
+
+    # ---- roofline of the dominant kernel (the sparse GEMM) ----
+    peaks = json.loads(PEAKS_FILE.read_text()) if PEAKS_FILE.exists() else {}
+    bf16_peak = peaks.get("bf16_tflops", 1590.0)
+    peak_basis = "measured" if "bf16_tflops" in peaks else "fallback"
+    sparse_peak = 2 * 2 * bf16_peak  # int8 dense = 2x bf16 (datasheet ratio); 2:4 sparse pipe = 2x dense
+    exec_flops = sum(2.0 * m * L.n * L.kp for L in layers)  # dense-equivalent ops run on the sparse pipe
+    gemm_ms = sum(sp_gemm)
+    achieved = exec_flops / (gemm_ms * 1e-3) / 1e12
+    traffic = None
+    if TRAFFIC_FILE.exists():
+        tr = json.loads(TRAFFIC_FILE.read_text())
+        traffic = tr.get("sparse_gemm_bytes_per_launch")
+    roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": round(sparse_peak, 1),
+                "unit": "TFLOP/s", "frac": round(achieved / sparse_peak, 4), "traffic": traffic,
+                "kernel": "gemm_kernel<sparse,i8> (tcgen05.mma.sp cta_group::2)",
+                "peak_basis": f"{peak_basis} bf16 {bf16_peak} TF x2 (int8/bf16 datasheet ratio) x2 (2:4 sparse pipe)",
+                "frac_of_datasheet_9000": round(achieved / 9000.0, 4),
+                "effective_tflops_gemm_only": round(sum(L.flops for L in layers) / (gemm_ms * 1e-3) / 1e12, 1)}
+    lift_bytes = sum(m * (2 * L.k + L.kp + 4) for L in layers)
+    lift_ms = sum(sp_lift)
+    lift_roofline = {"bound": "hbm", "achieved": round(lift_bytes / (lift_ms * 1e-3) / 1e9, 1),
+                     "peak": peaks.get("hbm_gbs", 6650.0), "unit": "GB/s",
+                     "frac": round(lift_bytes / (lift_ms * 1e-3) / 1e9 / peaks.get("hbm_gbs", 6650.0), 4)}
+
+    # ---- e2e through the public C-ABI with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(slsp, torch, layers, xs, outs, out_mode, z, l, stream, device, args, world, total_flops,
+                      reduce_max)
+
+    layer_rows = []
+    for i, L in enumerate(layers):
+        row = {"name": L.name, "n": L.n_total, "n_shard": L.n, "k": L.k, "kp": L.kp,
+               "lift_ms": round(sp_lift[i], 4), "sparse_gemm_ms": round(sp_gemm[i], 4),
+               "sparse_gemm_eff_tflops": round(L.flops / (sp_gemm[i] * 1e-3) / 1e12, 1)}
+        if de_gemm:
+            row.update({"quant_ms": round(de_lift[i], 4), "dense_gemm_ms": round(de_gemm[i], 4),
+                        "dense_gemm_tflops": round(L.flops / (de_gemm[i] * 1e-3) / 1e12, 1),
+                        "gemm_speedup": round(de_gemm[i] / sp_gemm[i], 4)})
+        layer_rows.append(row)
+
+    result = {
+        "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(sp_ms_max, 4), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "int8",
+        "data": "synthetic: W = magnitude_prune(U[-127,127], 6:8) int8 + per-channel fp32 scales, "
+                "X = U(-1,1) bf16, seeded",
+        "config": {"workload": f"{args.workload} all linear shapes, {args.pattern} INT8 W8A8, M={m} prefill",
+                   "m": m, "pattern": args.pattern, "layers": [f"{n}x{k}" for _, n, k in WORKLOADS[args.workload]],
+                   "step": "per layer: fused_quant_slide(bf16 X) + sparse GEMM, bf16 dequant epilogue",
+                   "out_layout": args.out_mode, "parallelism": f"N-shard x{world}" if world > 1 else "single",
+                   "l2": "flushed between timed steps (512 MiB write, outside events)"},
+        "speedup_vs_dense": round(de_ms_max / sp_ms_max, 4) if de_ms_max else None,
+        "gemm_speedup_vs_dense": round(sum(de_gemm) / sum(sp_gemm), 4) if de_gemm else None,
+        "speedup_bound": round(2 * sum(L.k for L in layers) / sum(L.kp for L in layers), 4),
+        "dense": {"value": round(dense_value, 2) if dense_value else None,
+                  "ms_per_step": round(de_ms_max, 4) if de_ms_max else None,
+                  "kernel": "gemm_kernel<dense,i8> (tcgen05.mma kind::i8 cta_group::2), our own"},
+        "roofline": roofline, "lift_roofline": lift_roofline, "layers": layer_rows,
+        "e2e": e2e, "clocks": clocks.result(),
+        "gpu_launches": 2 * len(layers) * args.steps,
+    }
+    if allgather:
+        result["allgather"] = allgather
+    if rank == 0 and world == 1 and not args.no_cpu:
+        result["cpu_baseline"] = cpu_baseline(slsp, torch, layers, xs, z, l, args.cpu_rows)
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def run_e2e(slsp, torch, layers, xs, outs, out_mode, z, l, stream, device, args, world, total_flops, reduce_max):
+    """Same step through the C ABI with HOST buffers: pinned H2D of each
+    layer's input, lift + sparse GEMM, D2H of each layer's BF16 output."""
+    host_x = {k: x.cpu().pin_memory() for k, x in xs.items()}
+    host_y = [torch.empty(o.shape, dtype=o.dtype, pin_memory=True) for o in outs]
+    dev_x = {k: torch.empty_like(x) for k, x in xs.items()}
+    steps = max(1, min(args.steps, 5))
+    h2d = sum(x.numel() * x.element_size() for L in layers for x in [host_x[L.k]])
+    d2h = sum(y.numel() * y.element_size() for y in host_y)
+
+    def step():
+        for i, L in enumerate(layers):
+            dev_x[L.k].copy_(host_x[L.k], non_blocking=True)
+            slsp.fused_quant_slide(dev_x[L.k], z, l, kp=L.kp, check=False, payload=L.payload, scales=L.s_tok)
+            slsp.sparse_gemm(L.packed, L.payload, s_ch=L.s_ch, s_tok=L.s_tok, out_mode=out_mode, out=outs[i])
+            host_y[i].copy_(outs[i], non_blocking=True)
+
+    step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = reduce_max(e0.elapsed_time(e1) / steps)
+    return {"value": round(total_flops / (ms * 1e-3) / 1e12, 3), "unit": UNIT, "ms_per_step": round(ms, 3),
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": steps,
+            "path": "slsp_fused_quant_slide + slsp_sparse_gemm (C ABI), pinned host in/out, one stream"}
+
+
+def _cpu_sample(R, torch, slsp, layers, xs, z, l, rows, threads):
+    """Bounded CPU sample of the same workload: for every layer, the
+    reference's fused_quant_slide over all M tokens plus its packed-word
+    sparse_gemm (gemm.hpp:199-233) over the first `rows` weight rows."""
+    import numpy as np
+
+    from oracle_lib import DT_BF16, KIND_INT8
+
+    work = []
+    for L in layers:
+        r = min(rows, L.n)
+        wsub = L.w[:r] if L.w is not None else None
+        if wsub is None:
+            raise RuntimeError("cpu baseline needs the dense weights (run without --no-dense)")
+        vals, codes = slsp.compress(slsp.pack_matrix(wsub.contiguous(), z, l))
+        x = xs[L.k].view(torch.int16).cpu().numpy().view(np.uint16)
+        work.append((vals.cpu().numpy(), codes.cpu().numpy(), x, r, L))
+    t0 = time.perf_counter()
+    flops = 0.0
+    for vals, codes, x, r, L in work:
+        payload, _ = R.fused_quant_slide(x, z, l, KIND_INT8, DT_BF16, threads=threads)
+        R.sparse_gemm_words(vals, codes, payload, threads=threads)
+        flops += 2.0 * r * L.m * L.k
+    dt = time.perf_counter() - t0
+    return flops, dt
+
+
+def cpu_baseline(slsp, torch, layers, xs, z, l, rows):
+    sys.path.insert(0, str(ROOT / "tests"))
+    from oracle_lib import orc, ref
+
+    R = ref()
+    kind = "reference"
+    if R is None:
+        R, kind = orc(), "port"
+    threads = os.cpu_count() or 1
+    flops, dt = _cpu_sample(R, torch, slsp, layers, xs, z, l, rows, threads)
+    return {"value": round(flops / dt / 1e12, 6), "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"per layer: fused_quant_slide over all {layers[0].m} tokens + packed-word sparse_gemm over "
+                      f"the first {rows} weight rows; {dt:.1f} s wall on {threads} threads",
+            "seconds": round(dt, 2)}
+
+
+def run_reference(args, world, rank, local):
+    """--impl reference: the reference's own CPU implementation (oracle/_ref,
+    the reference headers compiled unmodified) on this box's host cores, on a
+    bounded sample of the same workload per step. Rank 0 only."""
+    if rank != 0:
+        return
+    import numpy as np
+
+    sys.path.insert(0, str(ROOT / "tests"))
+    from oracle_lib import DT_BF16, DT_I8, KIND_INT8, orc, ref
+
+    R = ref()
+    kind = "reference"
+    if R is None:
+        R, kind = orc(), "port"
+    z, l = (int(v) for v in args.pattern.split(":"))
+    m = args.m
+    rows = max(1, args.cpu_rows // 4)
+    rng = np.random.default_rng(1234)
+    threads = os.cpu_count() or 1
+    work = []
+    for name, n, k in WORKLOADS[args.workload]:
+        w = R.magnitude_prune(rng.integers(-127, 128, size=(rows, k)).astype(np.int8), z, l, DT_I8)
+        vals, codes = R.compress(R.pack_matrix(w, z, l, DT_I8, threads=threads), DT_I8)
+        x = rng.uniform(-1, 1, size=(m, k)).astype(np.float32)
+        xb = ((x.view(np.uint32).astype(np.uint64) + 0x7FFF + ((x.view(np.uint32) >> 16) & 1)) >> 16).astype(np.uint16)
+        work.append((vals, codes, xb, k))
+
+    def step():
+        for vals, codes, xb, k in work:
+            payload, _ = R.fused_quant_slide(xb, z, l, KIND_INT8, DT_BF16, threads=threads)
+            R.sparse_gemm_words(vals, codes, payload, threads=threads)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = (time.perf_counter() - t0) / args.steps
+    flops = sum(2.0 * rows * m * k for *_, k in work)
+    value = flops / dt / 1e12
+    sample = (f"per layer of {args.workload}: fused_quant_slide over all {m} tokens + packed-word sparse_gemm "
+              f"over {rows} weight rows (of {', '.join(str(n) for _, n, _ in WORKLOADS[args.workload])})")
+    print(json.dumps({
+        "metric": METRIC, "value": round(value, 6), "unit": UNIT, "impl": "reference", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "int8",
+        "data": "synthetic: W = magnitude_prune(U[-127,127], 6:8) int8, X = U(-1,1) bf16, seeded",
+        "config": {"workload": f"{args.workload} all linear shapes, {args.pattern} INT8 W8A8, M={m} prefill",
+                   "m": m, "pattern": args.pattern, "sampled_rows_per_layer": rows},
+        "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
+        "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    args = parse_args()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, world, rank, local)
+    else:
+        run_b200(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -256,14 +256,17 @@ def _in_dtype(x: torch.Tensor) -> int:
 
 
 def fused_quant_slide(x: torch.Tensor, z: int, l: int, kind: int = QUANT_INT8, kp: int | None = None,
-                      check: bool = True) -> tuple[torch.Tensor, torch.Tensor]:
+                      check: bool = True, payload: torch.Tensor | None = None,
+                      scales: torch.Tensor | None = None) -> tuple[torch.Tensor, torch.Tensor]:
     """quantize.hpp:122-174 -> (payload rows x kp/4 uint32 words as int32 storage, scales fp32)."""
     _require_cuda(x)
     rows, cols = x.shape
     kprime = lifted_width(cols, z, l)
     kp = round_up(kprime, 256) if kp is None else kp
-    payload = torch.empty((rows, kp // 4), dtype=torch.int32, device=x.device)
-    scales = torch.empty(rows, dtype=torch.float32, device=x.device)
+    if payload is None:
+        payload = torch.empty((rows, kp // 4), dtype=torch.int32, device=x.device)
+    if scales is None:
+        scales = torch.empty(rows, dtype=torch.float32, device=x.device)
     bad = C.c_int64(-1)
     ws = _status_ws(x.device) if check else None
     st = lib().slsp_fused_quant_slide(_in_dtype(x), _ptr(x), rows, cols, z, l, kind, kp, _ptr(payload),
@@ -274,13 +277,16 @@ def fused_quant_slide(x: torch.Tensor, z: int, l: int, kind: int = QUANT_INT8, k
 
 
 def quantize_rows(x: torch.Tensor, kind: int = QUANT_INT8, kpad: int | None = None,
-                  check: bool = True) -> tuple[torch.Tensor, torch.Tensor]:
+                  check: bool = True, out: torch.Tensor | None = None,
+                  scales: torch.Tensor | None = None) -> tuple[torch.Tensor, torch.Tensor]:
     """quantize.hpp:52-68 quantize_row for every token row -> (bytes rows x kpad, scales)."""
     _require_cuda(x)
     rows, cols = x.shape
     kpad = round_up(cols, 128) if kpad is None else kpad
-    out = torch.empty((rows, kpad), dtype=torch.uint8, device=x.device)
-    scales = torch.empty(rows, dtype=torch.float32, device=x.device)
+    if out is None:
+        out = torch.empty((rows, kpad), dtype=torch.uint8, device=x.device)
+    if scales is None:
+        scales = torch.empty(rows, dtype=torch.float32, device=x.device)
     bad = C.c_int64(-1)
     ws = _status_ws(x.device) if check else None
     st = lib().slsp_quantize_rows(_in_dtype(x), _ptr(x), rows, cols, kind, kpad, _ptr(out), _ptr(scales),

@@ -12,13 +12,15 @@
 //               and tcgen05.mma[.sp] (M=256 across the pair, N=BN tokens);
 //               both CTAs: TMEM allocation.
 //   warps 2-5   epilogue (both CTAs): tcgen05.ld the accumulator lanes,
-//               optional per-channel x per-token dequant to BF16, stores.
+//               optional per-channel x per-token dequant to BF16, swizzled
+//               smem staging, TMA bulk tensor stores.
 // Accumulators are double-buffered in TMEM so the epilogue of tile i overlaps
 // the mainloop of tile i+1. The weight (sparse) operand is A: MMA-M = output
 // features, MMA-N = tokens.
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <mutex>
-#include <unordered_map>
 
 #include "common.cuh"
 #include "internal.h"
@@ -28,7 +30,11 @@ namespace {
 using namespace slsp_dev;
 
 constexpr int kNumThreads = 192;
-constexpr int kEpiWarp0 = 2;
+
+// Debug knobs (env SLSP_GEMM_DEBUG, read once): bit0 skip output stores,
+// bit1 skip operand loads (MMA on stale smem), bit2 load k-block 0 of tile 0
+// only (L2-resident operands). Results are garbage when set; perf probing only.
+enum : uint32_t { kDbgNoStore = 1u, kDbgNoLoad = 2u, kDbgSameTile = 4u };
 
 template <bool SPARSE_, MmaKind KIND_, int BN_, int STAGES_, int OUT_>
 struct Cfg {
@@ -54,12 +60,19 @@ struct Cfg {
   static_assert(!SPARSE || E_COL + 8 <= TMEM_COLS, "TMEM budget: 2 accumulators + metadata");
   static_assert(SPARSE || 2 * BN <= TMEM_COLS, "TMEM budget: 2 accumulators");
   static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "cta_group::2 N");
+  // epilogue staging: per warp, EPI_BUFS tiles of 32 rows x 32 columns
+  static constexpr int OUT_ESZ = OUT == SLSP_OUT_RAW_NM ? 4 : 2;
+  static constexpr int EPI_BUFS = OUT == SLSP_OUT_RAW_NM ? 1 : 2;
+  static constexpr int EPI_BUF = 32 * 32 * OUT_ESZ;
+  static constexpr int EPI_WARP = EPI_BUFS * EPI_BUF;
   static constexpr int OFF_A = 0;
   static constexpr int OFF_B = OFF_A + STAGES * A_STAGE;
   static constexpr int OFF_E = OFF_B + STAGES * B_STAGE;
-  static constexpr int OFF_BAR = OFF_E + STAGES * E_STAGE;
+  static constexpr int OFF_EPI = OFF_E + STAGES * E_STAGE;
+  static constexpr int OFF_BAR = OFF_EPI + 4 * EPI_WARP;
   static constexpr int NUM_BARS = 2 * STAGES + 4;
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16 + 1024;  // + alignment slack
+  static_assert(SMEM <= 227 * 1024, "shared memory budget");
   static constexpr uint32_t C_FMT = KIND == MmaKind::I8 ? 2u : 1u;
   static constexpr uint32_t AB_FMT = KIND == MmaKind::F8 ? 0u : 1u;
   static constexpr uint32_t IDESC = make_idesc(SPARSE, C_FMT, AB_FMT, AB_FMT, BM, BN);
@@ -74,6 +87,8 @@ struct Params {
   const float* s_tok; // per token
   void* out;
   int64_t ldo;
+  int tma_store;      // 1: swizzled smem staging + TMA store; 0: direct stores
+  uint32_t debug;
 };
 
 SLSP_DEVINL void tile_coords(int tile, int m_tiles, int n_tiles, int& mt, int& nt) {
@@ -87,59 +102,104 @@ SLSP_DEVINL void tile_coords(int tile, int m_tiles, int n_tiles, int& mt, int& n
   nt = r / gsize;
 }
 
+// a18: y = bf16((acc * s_ch[n]) * s_tok[t]) — fp32, this exact operation order
+// (restated by oracle/slsp_oracle.c orc_dequant_bf16).
+template <typename Acc>
+SLSP_DEVINL float dequant(uint32_t raw, float sc, float st) {
+  float a;
+  if constexpr (std::is_same<Acc, int32_t>::value) a = __int2float_rn(static_cast<int32_t>(raw));
+  else a = __uint_as_float(raw);
+  return __fmul_rn(__fmul_rn(a, sc), st);
+}
+
+SLSP_DEVINL uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// One 32-row x 32-column chunk of the accumulator (lane = row) to its output.
 template <typename C>
-SLSP_DEVINL void epilogue_store(const Params& p, const uint32_t (&r)[32], int64_t row, int64_t t0) {
-  using Acc = typename C::Acc;
+SLSP_DEVINL void epilogue_chunk(const Params& p, const CUtensorMap* tmOut, uint8_t* stage, uint32_t (&r)[32],
+                                int64_t row0, int64_t t0, float sc) {
+  const uint32_t lane = lane_id();
+  const int64_t row = row0 + lane;
+  // per-token scales: one coalesced load, shuffled to every lane
+  float st_lane = 0.f;
+  if constexpr (C::OUT != SLSP_OUT_RAW_NM) st_lane = (t0 + lane < p.m) ? __ldg(p.s_tok + t0 + lane) : 0.f;
+  uint32_t w[C::OUT == SLSP_OUT_RAW_NM ? 32 : 16];  // packed output words of this lane's row
+  if constexpr (C::OUT == SLSP_OUT_RAW_NM) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) w[i] = r[i];
+  } else {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const float lo = dequant<typename C::Acc>(r[2 * i], sc, __shfl_sync(0xffffffffu, st_lane, 2 * i));
+      const float hi = dequant<typename C::Acc>(r[2 * i + 1], sc, __shfl_sync(0xffffffffu, st_lane, 2 * i + 1));
+      w[i] = pack_bf16(lo, hi);
+    }
+  }
+  if (p.debug & kDbgNoStore) return;
+
+  if (p.tma_store) {
+    const uint32_t sb = smem_u32(stage);
+    if constexpr (C::OUT == SLSP_OUT_BF16_MN) {
+      // token-major tile [32 tokens][32 features] bf16, 64B rows, 64B swizzle
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const uint32_t chunk = (lane >> 3) ^ ((i >> 1) & 3);
+        const uint16_t v = static_cast<uint16_t>(w[i >> 1] >> (16 * (i & 1)));
+        st_shared_u16(sb + i * 64 + chunk * 16 + (lane & 7) * 2, v);
+      }
+    } else if constexpr (C::OUT_ESZ == 2) {
+      // [32 rows][32 tokens] bf16: 64B rows, 64B swizzle (chunk ^= (row>>1)&3)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        st_shared_v4(sb + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4), w[4 * j], w[4 * j + 1], w[4 * j + 2],
+                     w[4 * j + 3]);
+    } else {
+      // [32 rows][32 tokens] 32-bit: 128B rows, 128B swizzle (chunk ^= row&7)
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        st_shared_v4(sb + lane * 128 + ((j ^ (lane & 7)) << 4), w[4 * j], w[4 * j + 1], w[4 * j + 2],
+                     w[4 * j + 3]);
+    }
+    fence_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      if constexpr (C::OUT == SLSP_OUT_BF16_MN)
+        tma_store_2d(tmOut, stage, static_cast<int>(row0), static_cast<int>(t0));
+      else
+        tma_store_2d(tmOut, stage, static_cast<int>(t0), static_cast<int>(row0));
+      bulk_commit();
+    }
+    return;
+  }
+  // direct stores (unaligned output strides): predicated, register-resident
   if (row >= p.n) return;
-  const int valid = static_cast<int>(imin64(32, p.m - t0));
-  if (valid <= 0) return;
+  const int64_t valid = imin64(32, p.m - t0);
   if constexpr (C::OUT == SLSP_OUT_RAW_NM) {
     uint32_t* dst = reinterpret_cast<uint32_t*>(p.out) + row * p.ldo + t0;
-    if (valid == 32 && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
-        reinterpret_cast<uint4*>(dst)[i] = make_uint4(r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
-    } else {
-      for (int i = 0; i < valid; ++i) dst[i] = r[i];
-    }
+    for (int i = 0; i < 32; ++i)
+      if (i < valid) dst[i] = w[i];
+  } else if constexpr (C::OUT == SLSP_OUT_BF16_NM) {
+    uint16_t* dst = reinterpret_cast<uint16_t*>(p.out) + row * p.ldo + t0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (i < valid) dst[i] = static_cast<uint16_t>(w[i >> 1] >> (16 * (i & 1)));
   } else {
-    const float sc = __ldg(p.s_ch + row);
-    float y[32];
+    uint16_t* dst = reinterpret_cast<uint16_t*>(p.out) + t0 * p.ldo + row;
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      float a;
-      if constexpr (std::is_same<Acc, int32_t>::value) a = __int2float_rn(static_cast<int32_t>(r[i]));
-      else a = __uint_as_float(r[i]);
-      const float st = (t0 + i < p.m) ? __ldg(p.s_tok + t0 + i) : 0.f;
-      y[i] = __fmul_rn(__fmul_rn(a, sc), st);
-    }
-    if constexpr (C::OUT == SLSP_OUT_BF16_NM) {
-      __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.out) + row * p.ldo + t0;
-      if (valid == 32 && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          uint32_t w[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            __nv_bfloat162 h = __floats2bfloat162_rn(y[8 * i + 2 * j], y[8 * i + 2 * j + 1]);
-            w[j] = *reinterpret_cast<uint32_t*>(&h);
-          }
-          reinterpret_cast<uint4*>(dst)[i] = make_uint4(w[0], w[1], w[2], w[3]);
-        }
-      } else {
-        for (int i = 0; i < valid; ++i) dst[i] = __float2bfloat16_rn(y[i]);
-      }
-    } else {  // SLSP_OUT_BF16_MN: lanes hold consecutive features -> coalesced per token
-      __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.out) + t0 * p.ldo + row;
-      for (int i = 0; i < valid; ++i) dst[i * p.ldo] = __float2bfloat16_rn(y[i]);
-    }
+    for (int i = 0; i < 32; ++i)
+      if (i < valid) dst[i * p.ldo] = static_cast<uint16_t>(w[i >> 1] >> (16 * (i & 1)));
   }
 }
 
 template <typename C>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                const __grid_constant__ CUtensorMap tmE, const Params p) {
+                const __grid_constant__ CUtensorMap tmE, const __grid_constant__ CUtensorMap tmOut,
+                const Params p) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -174,6 +234,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
     if (C::SPARSE) tma_prefetch(&tmE);
+    if (p.tma_store) tma_prefetch(&tmOut);
   }
   if (warp == 1) tmem_alloc<2>(tmem_slot, C::TMEM_COLS);
   tc_fence_before();
@@ -186,21 +247,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
+      const bool no_load = p.debug & kDbgNoLoad;
+      const bool same = p.debug & kDbgSameTile;
       for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
         int mt, nt;
         tile_coords(tile, p.m_tiles, p.n_tiles, mt, nt);
+        if (same) mt = nt = 0;
         const int a_row = mt * C::BM + static_cast<int>(rank) * C::A_ROWS;
         const int b_row = nt * C::BN + static_cast<int>(rank) * C::B_ROWS;
         for (int kb = 0; kb < p.num_kb; ++kb) {
+          const int kl = same ? 0 : kb;
           mbar_wait(&empty[stage], phase ^ 1);
-          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_TX);
-          const uint32_t bar = mapa_shared(smem_u32(&full[stage]), 0);
-          tma_load_2d_cg2(sA + stage * C::A_STAGE, &tmA, bar, kb * 128, a_row);
+          if (no_load) {
+            if (leader) mbar_arrive(&full[stage]);
+          } else {
+            if (leader) mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_TX);
+            const uint32_t bar = mapa_shared(smem_u32(&full[stage]), 0);
+            tma_load_2d_cg2(sA + stage * C::A_STAGE, &tmA, bar, kl * 128, a_row);
 #pragma unroll
-          for (int at = 0; at < C::B_ATOMS; ++at)
-            tma_load_2d_cg2(sB + stage * C::B_STAGE + at * C::B_ATOM, &tmB, bar, kb * C::K_BYTES_B + at * 128,
-                            b_row);
-          if constexpr (C::SPARSE) tma_load_3d_cg2(sE + stage * C::E_STAGE, &tmE, bar, 0, a_row, kb * 2);
+            for (int at = 0; at < C::B_ATOMS; ++at)
+              tma_load_2d_cg2(sB + stage * C::B_STAGE + at * C::B_ATOM, &tmB, bar, kl * C::K_BYTES_B + at * 128,
+                              b_row);
+            if constexpr (C::SPARSE) tma_load_3d_cg2(sE + stage * C::E_STAGE, &tmE, bar, 0, a_row, kl * 2);
+          }
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
@@ -256,6 +325,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
     // ------------------------------------------------ epilogue ----
     const uint32_t quarter = warp & 3;  // TMEM lane quarter this warp may access
     const uint32_t lane = lane_id();
+    uint8_t* stage_base = smem + C::OFF_EPI + (warp - 2) * C::EPI_WARP;
+    int buf = 0;
     int it = 0;
     for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
       int mt, nt;
@@ -264,19 +335,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int64_t row = static_cast<int64_t>(mt) * C::BM + rank * C::A_ROWS + quarter * 32 + lane;
+      const int64_t row0 = static_cast<int64_t>(mt) * C::BM + rank * C::A_ROWS + quarter * 32;
+      float sc = 0.f;
+      if constexpr (C::OUT != SLSP_OUT_RAW_NM) sc = (row0 + lane < p.n) ? __ldg(p.s_ch + row0 + lane) : 0.f;
       const uint32_t t_base = tmem + ((quarter * 32) << 16) + acc * C::ACC_COLS;
 #pragma unroll 1
       for (int c = 0; c < C::BN / 32; ++c) {
+        const int64_t t0 = static_cast<int64_t>(nt) * C::BN + c * 32;
+        if (t0 >= p.m) break;  // warp-uniform
         uint32_t r[32];
         tmem_ld_32x32b_x32(t_base + c * 32, r);
         tmem_ld_wait();
-        epilogue_store<C>(p, r, row, static_cast<int64_t>(nt) * C::BN + c * 32);
+        if (p.tma_store) {
+          if (lane == 0) bulk_wait_read<C::EPI_BUFS - 1>();  // staging buffer free again
+          __syncwarp();
+        }
+        epilogue_chunk<C>(p, &tmOut, stage_base + buf * C::EPI_BUF, r, row0, t0, sc);
+        if (C::EPI_BUFS == 2) buf ^= 1;
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
     }
+    if (lane == 0) bulk_wait<0>();
   }
 
   tc_fence_before();
@@ -302,6 +383,14 @@ EncodeTiledFn get_encode() {
       fn = reinterpret_cast<EncodeTiledFn>(p);
   });
   return fn;
+}
+
+uint32_t debug_flags() {
+  static uint32_t flags = [] {
+    const char* e = std::getenv("SLSP_GEMM_DEBUG");
+    return e ? static_cast<uint32_t>(std::strtoul(e, nullptr, 0)) : 0u;
+  }();
+  return flags;
 }
 
 // Byte-addressed 2D map (uint8 elements): rows x row_bytes, box rows x 128 B, 128B swizzle.
@@ -333,6 +422,29 @@ int make_map_meta(CUtensorMap* map, const void* base, uint64_t rows, uint64_t kp
   return r == CUDA_SUCCESS ? SLSP_OK : SLSP_ERR_CUDA;
 }
 
+// Output map for the TMA-store epilogue: 32x32 element boxes.
+//   NM: (cols = tokens m, rows = n); MN: (cols = n, rows = tokens m).
+int make_map_out(CUtensorMap* map, void* base, int out_mode, int64_t n, int64_t m, int64_t ldo, int* use_tma) {
+  const int esz = out_mode == SLSP_OUT_RAW_NM ? 4 : 2;
+  *use_tma = 0;
+  std::memset(map, 0, sizeof(*map));
+  if ((reinterpret_cast<uintptr_t>(base) & 15u) || (ldo * esz) % 16) return SLSP_OK;  // direct-store path
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return SLSP_ERR_CUDA;
+  const bool mn = out_mode == SLSP_OUT_BF16_MN;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(mn ? n : m), static_cast<cuuint64_t>(mn ? m : n)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldo * esz)};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, base, dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   esz == 4 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return SLSP_ERR_CUDA;
+  *use_tma = 1;
+  return SLSP_OK;
+}
+
 int num_sms() {
   static int sms = 0;
   if (!sms) {
@@ -344,7 +456,8 @@ int num_sms() {
 }
 
 template <typename C>
-int run(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, Params p, cudaStream_t s) {
+int run(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const CUtensorMap& o, Params p,
+        cudaStream_t s) {
   static bool configured = false;
   auto kern = gemm_kernel<C>;
   if (!configured) {
@@ -356,19 +469,24 @@ int run(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, Params
   const int tiles = p.m_tiles * p.n_tiles;
   if (tiles == 0) return SLSP_OK;
   int clusters = num_sms() / 2;
+  static const int cluster_cap = [] {
+    const char* e = std::getenv("SLSP_GEMM_CLUSTERS");  // perf probing: cap the persistent grid
+    return e ? std::atoi(e) : 0;
+  }();
+  if (cluster_cap > 0 && clusters > cluster_cap) clusters = cluster_cap;
   if (clusters > tiles) clusters = tiles;
-  kern<<<2 * clusters, kNumThreads, C::SMEM, s>>>(a, b, e, p);
+  kern<<<2 * clusters, kNumThreads, C::SMEM, s>>>(a, b, e, o, p);
   SLSP_LAUNCH_CHECK();
   return SLSP_OK;
 }
 
 template <bool SPARSE, MmaKind K, int BN, int ST>
-int run_out(int out_mode, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const Params& p,
-            cudaStream_t s) {
+int run_out(int out_mode, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const CUtensorMap& o,
+            const Params& p, cudaStream_t s) {
   switch (out_mode) {
-    case SLSP_OUT_RAW_NM: return run<Cfg<SPARSE, K, BN, ST, SLSP_OUT_RAW_NM>>(a, b, e, p, s);
-    case SLSP_OUT_BF16_NM: return run<Cfg<SPARSE, K, BN, ST, SLSP_OUT_BF16_NM>>(a, b, e, p, s);
-    case SLSP_OUT_BF16_MN: return run<Cfg<SPARSE, K, BN, ST, SLSP_OUT_BF16_MN>>(a, b, e, p, s);
+    case SLSP_OUT_RAW_NM: return run<Cfg<SPARSE, K, BN, ST, SLSP_OUT_RAW_NM>>(a, b, e, o, p, s);
+    case SLSP_OUT_BF16_NM: return run<Cfg<SPARSE, K, BN, ST, SLSP_OUT_BF16_NM>>(a, b, e, o, p, s);
+    case SLSP_OUT_BF16_MN: return run<Cfg<SPARSE, K, BN, ST, SLSP_OUT_BF16_MN>>(a, b, e, o, p, s);
   }
   return SLSP_ERR_INVALID;
 }
@@ -409,11 +527,12 @@ int slsp_sparse_gemm(int dtype, const void* values, const uint8_t* meta, int64_t
   if (dtype != SLSP_DT_I8 && dtype != SLSP_DT_E4M3) return SLSP_ERR_UNSUPPORTED;
   if ((st = require_sm100())) return st;
   if (n == 0 || m == 0) return SLSP_OK;
-  CUtensorMap ta, tb, te;
+  CUtensorMap ta, tb, te, to;
+  Params p{};
   if ((st = make_map_2d(&ta, values, kp / 2, n, 128))) return st;
   if ((st = make_map_2d(&tb, act, kp, m, kSparseBN / 2))) return st;
   if ((st = make_map_meta(&te, meta, n, kp))) return st;
-  Params p{};
+  if ((st = make_map_out(&to, out, out_mode, n, m, ldo, &p.tma_store))) return st;
   p.n = n;
   p.m = m;
   p.num_kb = static_cast<int>(kp / 256);
@@ -421,9 +540,10 @@ int slsp_sparse_gemm(int dtype, const void* values, const uint8_t* meta, int64_t
   p.s_tok = s_tok;
   p.out = out;
   p.ldo = ldo;
+  p.debug = debug_flags();
   if (dtype == SLSP_DT_I8)
-    return run_out<true, MmaKind::I8, kSparseBN, kSparseStages>(out_mode, ta, tb, te, p, s);
-  return run_out<true, MmaKind::F8, kSparseBN, kSparseStages>(out_mode, ta, tb, te, p, s);
+    return run_out<true, MmaKind::I8, kSparseBN, kSparseStages>(out_mode, ta, tb, te, to, p, s);
+  return run_out<true, MmaKind::F8, kSparseBN, kSparseStages>(out_mode, ta, tb, te, to, p, s);
 }
 
 int slsp_dense_gemm(int dtype, const void* w, int64_t n, int64_t k, const void* act, int64_t m, const float* s_ch,
@@ -440,11 +560,11 @@ int slsp_dense_gemm(int dtype, const void* w, int64_t n, int64_t k, const void* 
   if (st) return st;
   if ((st = require_sm100())) return st;
   if (n == 0 || m == 0) return SLSP_OK;
-  CUtensorMap ta, tb, te;
+  CUtensorMap ta, tb, to;
+  Params p{};
   if ((st = make_map_2d(&ta, w, k * esz, n, 128))) return st;
   if ((st = make_map_2d(&tb, act, k * esz, m, kDenseBN / 2))) return st;
-  te = ta;
-  Params p{};
+  if ((st = make_map_out(&to, out, out_mode, n, m, ldo, &p.tma_store))) return st;
   p.n = n;
   p.m = m;
   p.num_kb = static_cast<int>(k * esz / 128);
@@ -452,9 +572,12 @@ int slsp_dense_gemm(int dtype, const void* w, int64_t n, int64_t k, const void* 
   p.s_tok = s_tok;
   p.out = out;
   p.ldo = ldo;
-  if (dtype == SLSP_DT_I8) return run_out<false, MmaKind::I8, kDenseBN, kDenseStages>(out_mode, ta, tb, te, p, s);
-  if (dtype == SLSP_DT_E4M3) return run_out<false, MmaKind::F8, kDenseBN, kDenseStages>(out_mode, ta, tb, te, p, s);
-  return run_out<false, MmaKind::F16, kDenseBN, kDenseStages>(out_mode, ta, tb, te, p, s);
+  p.debug = debug_flags();
+  if (dtype == SLSP_DT_I8)
+    return run_out<false, MmaKind::I8, kDenseBN, kDenseStages>(out_mode, ta, tb, ta, to, p, s);
+  if (dtype == SLSP_DT_E4M3)
+    return run_out<false, MmaKind::F8, kDenseBN, kDenseStages>(out_mode, ta, tb, ta, to, p, s);
+  return run_out<false, MmaKind::F16, kDenseBN, kDenseStages>(out_mode, ta, tb, ta, to, p, s);
 }
 
 }  // extern "C"

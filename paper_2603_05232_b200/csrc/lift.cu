@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(kThreads) act_kernel(ActArgs a) {
       amax = fmaxf(amax, s_red[i]);
       bad |= s_bad[i];
     }
-    if (bad && threadIdx.x == 0) atomicMin(a.status, static_cast<unsigned long long>(row) << 32);
+    if (bad && threadIdx.x == 0 && a.status) atomicMin(a.status, static_cast<unsigned long long>(row) << 32);
 
     if constexpr (KIND != K_NONE) {
       // quantize.hpp:151-153: r = qmax/absmax, scale = float(absmax/qmax), in double.
@@ -180,12 +180,21 @@ int launch_act(ActArgs& a, int esz, cudaStream_t s) {
   const size_t smem = ((a.in_cols_pad * esz + 15) & ~static_cast<int64_t>(15)) + (KIND != K_NONE ? a.in_cols_pad : 0);
   if (smem > 200 * 1024) return SLSP_ERR_UNSUPPORTED;
   auto k = act_kernel<IN, KIND, LIFT>;
-  SLSP_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  int per_sm = 1;
-  SLSP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, smem));
-  int dev = 0, sms = 148;
-  SLSP_CUDA_TRY(cudaGetDevice(&dev));
-  SLSP_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  // Launch configuration is cached per kernel instance and smem size so the
+  // entry point stays cheap and CUDA-graph capturable (no per-call queries).
+  static size_t cached_smem = 0;
+  static int cached_per_sm = 0, sms = 0;
+  if (!sms) {
+    int dev = 0;
+    SLSP_CUDA_TRY(cudaGetDevice(&dev));
+    SLSP_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    SLSP_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  }
+  if (cached_smem != smem) {
+    SLSP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cached_per_sm, k, kThreads, smem));
+    cached_smem = smem;
+  }
+  const int per_sm = cached_per_sm;
   const int64_t cap = static_cast<int64_t>(sms) * (per_sm > 0 ? per_sm : 1);
   const unsigned grid = static_cast<unsigned>(a.rows < cap ? a.rows : cap);
   k<<<grid, kThreads, smem, s>>>(a);
@@ -204,23 +213,14 @@ int dispatch_quant(int in_dtype, int kind, ActArgs& a, cudaStream_t s) {
                                  : launch_act<IN_BF16, K_FP8, LIFT>(a, esz, s);
 }
 
-// Scratch for the mandatory-in-kernel status word when the caller skips checks.
+// Status word: the caller's scratch when checking, else none (kernels skip
+// the report; the hot path stays asynchronous and graph-capturable).
 struct StatusScope {
   unsigned long long* ptr = nullptr;
-  unsigned long long* owned = nullptr;
-  cudaStream_t s{};
   int init(void* ws, cudaStream_t st) {
-    s = st;
-    if (ws) {
-      ptr = static_cast<unsigned long long*>(ws);
-      return slsp_host::status_reset(ws, st);
-    }
-    SLSP_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&owned), sizeof(unsigned long long), st));
-    ptr = owned;
-    return SLSP_OK;
-  }
-  ~StatusScope() {
-    if (owned) cudaFreeAsync(owned, s);
+    if (!ws) return SLSP_OK;
+    ptr = static_cast<unsigned long long*>(ws);
+    return slsp_host::status_reset(ws, st);
   }
 };
 

@@ -42,7 +42,7 @@ SLSP_DEVINL void store_elem(uint8_t* base, int64_t idx, uint64_t v) {
 }
 
 SLSP_DEVINL void record_error(unsigned long long* status, int64_t row, int64_t index) {
-  atomicMin(status, (static_cast<unsigned long long>(row) << 32) | static_cast<unsigned long long>(index));
+  if (status) atomicMin(status, (static_cast<unsigned long long>(row) << 32) | static_cast<unsigned long long>(index));
 }
 
 // Block-cooperative copy smem -> global: 32-bit stores when the destination
@@ -246,8 +246,11 @@ int launch_pack(int esz, PackArgs& a, cudaStream_t s) {
 #define SLSP_PACK_LAUNCH(E)                                                                  \
   do {                                                                                       \
     auto k = pack_kernel<E, MODE>;                                                           \
-    if (smem > 48 * 1024)                                                                    \
-      SLSP_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    static bool attr_set = false;                                                            \
+    if (!attr_set) {                                                                         \
+      SLSP_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024)); \
+      attr_set = true;                                                                       \
+    }                                                                                        \
     k<<<grid, kThreads, smem, s>>>(a);                                                       \
   } while (0)
   switch (esz) {
@@ -317,12 +320,7 @@ int slsp_pack_compress(int dtype, const void* w, int64_t rows, int64_t cols, int
   if (kp < kprime || kp % 8 != 0) return SLSP_ERR_DIMENSION;
   if ((st = require_sm100())) return st;
   if ((st = status_reset(status_ws, s))) return st;
-  unsigned long long* status = static_cast<unsigned long long*>(status_ws);
-  unsigned long long* scratch = nullptr;
-  if (!status) {  // the kernel always reports; park reports in a throwaway word
-    SLSP_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&scratch), sizeof(unsigned long long), s));
-    status = scratch;
-  }
+  unsigned long long* status = static_cast<unsigned long long*>(status_ws);  // may be null: no report
   PackArgs a{};
   a.w = static_cast<const uint8_t*>(w);
   a.rows = rows;
@@ -339,9 +337,7 @@ int slsp_pack_compress(int dtype, const void* w, int64_t rows, int64_t cols, int
   a.ld_a_bytes = kp / 2 * esz;
   a.ld_meta = kp / 8;
   a.status = status;
-  st = launch_pack<1>(esz, a, s);
-  if (scratch) SLSP_CUDA_TRY(cudaFreeAsync(scratch, s));
-  if (st) return st;
+  if ((st = launch_pack<1>(esz, a, s))) return st;
   return status_collect(status_ws, s, SLSP_ERR_NOT_COMPLIANT, err_row, err_block);
 }
 

@@ -70,9 +70,20 @@ const char* slsp_status_string(int status) {
 const char* slsp_last_cuda_error(void) { return slsp_host::g_last_cuda_error; }
 
 int slsp_device_supported(int dev) {
-  cudaDeviceProp prop;
-  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) return 0;
-  return prop.major == 10 && prop.minor == 0;
+  // Cached per device: cudaGetDeviceProperties costs milliseconds and every
+  // entry point checks the architecture (kernels are sm_100a-only).
+  static int cache[64] = {0};  // 0 unknown, 1 supported, 2 not supported
+  if (dev < 0) return 0;
+  if (dev < 64 && cache[dev]) return cache[dev] == 1;
+  int major = 0, minor = 0;
+  if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  const int ok = major == 10 && minor == 0;
+  if (dev < 64) cache[dev] = ok ? 1 : 2;
+  return ok;
 }
 
 // pattern.hpp:107-117 plan_status, pattern.hpp:131-154 plan_decomposition.

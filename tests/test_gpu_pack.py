@@ -137,11 +137,11 @@ def test_compress_rejects_overfull_window(slsp):
 def test_magnitude_prune_matches_oracle(slsp, orc, dt):
     rng = np.random.default_rng(11)
     if dt == "i8":
-        w = rng.integers(-127, 128, size=(64, 256)).astype(np.int8)
+        w = rng.integers(-127, 128, size=(64, 240)).astype(np.int8)
         w[:, ::7] = w[:, 1::7][:, : w[:, ::7].shape[1]]  # magnitude ties
         code = DT_I8
     else:
-        w = rng.uniform(-1, 1, size=(64, 256)).astype(np.float32)
+        w = rng.uniform(-1, 1, size=(64, 240)).astype(np.float32)
         code = DT_F32
     for z, l in PATTERNS[:3]:
         got = slsp.magnitude_prune(dev(w), z, l).cpu().numpy()
