@@ -111,6 +111,18 @@ SLSP_API int slsp_pack_compress(int dtype, const void* w, int64_t rows, int64_t 
                        void* values, uint8_t* meta, void* status_ws, int64_t* err_row, int64_t* err_block,
                        slsp_stream_t stream);
 
+/* MMA-tiled metadata (the operand format of slsp_sparse_gemm): re-tiles the
+ * row-major codes (rows x kp/8 bytes, as written by slsp_pack_compress) into
+ * contiguous 4 KB blocks, one per (128-row block b, 256-wide k-stage s):
+ *   tiled[((b*(kp/256) + s)*2 + c)*2048 + r*16 + j] = meta[(b*128 + r)*(kp/8) + s*32 + c*16 + j]
+ * i.e. two 128x16-byte tcgen05.cp atoms per stage. Rows past `rows` up to the
+ * next multiple of 128 are filled with canonical codes (0,1) = 0x44. `tiled`
+ * holds ceil(rows/128)*128 * kp/8 bytes. kp % 256 == 0. */
+SLSP_API int slsp_tile_meta(const uint8_t* meta, int64_t rows, int64_t kp, uint8_t* tiled, slsp_stream_t stream);
+
+/* Bytes of the tiled metadata buffer for `rows` x `kp`. */
+SLSP_API int64_t slsp_tiled_meta_bytes(int64_t rows, int64_t kp);
+
 /* a8 — pack.hpp:238-261 magnitude_prune (synthesises compliant weights). */
 SLSP_API int slsp_magnitude_prune(int dtype, const void* w, int64_t rows, int64_t cols, int z, int l, void* out,
                          slsp_stream_t stream);
@@ -138,7 +150,8 @@ SLSP_API int slsp_lift_rows(int dtype, const void* x, int64_t rows, int64_t cols
  *   dtype I8  : values int8,  act = quantized payload bytes (int8), acc int32
  *   dtype E4M3: values e4m3,  act = e4m3 payload bytes,              acc fp32
  *   dtype BF16: values bf16,  act = lifted bf16,                     acc fp32
- * values: n x kp/2, meta: n x kp/8 (slsp_pack_compress format), act: m x kp.
+ * values: n x kp/2 (slsp_pack_compress), meta: the slsp_tile_meta layout
+ * (slsp_tiled_meta_bytes(n, kp) bytes), act: m x kp.
  * kp % 256 == 0. s_ch (n) / s_tok (m) are required for the BF16 outputs.
  * out: SLSP_OUT_RAW_NM / BF16_NM -> n x m (row stride ldo elements);
  *      SLSP_OUT_BF16_MN -> m x n (row stride ldo). */

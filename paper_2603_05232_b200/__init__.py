@@ -9,7 +9,7 @@ from ._native import (  # noqa: F401
     CudaError, DimensionMismatchError, MalformedMetadataError, NonFiniteInputError, NotCompliantError,
     PackedWeights, PlanError, SlspError, UnsupportedError, compress, dense_gemm, device_supported,
     fused_quant_slide, lib, lift_rows, lifted_width, magnitude_prune, pack_compress, pack_matrix,
-    plan_decomposition, quantize_rows, round_up, sparse_gemm,
+    plan_decomposition, quantize_rows, round_up, sparse_gemm, tile_meta,
 )
 
 __version__ = "0.1.0"

@@ -101,6 +101,8 @@ def lib() -> C.CDLL:
                 "slsp_lift_rows": (i32, [i32, vp, i64, i64, i32, i32, i64, vp, vp]),
                 "slsp_sparse_gemm": (i32, [i32, vp, vp, i64, i64, vp, i64, vp, vp, i32, vp, i64, vp]),
                 "slsp_dense_gemm": (i32, [i32, vp, i64, i64, vp, i64, vp, vp, i32, vp, i64, vp]),
+                "slsp_tile_meta": (i32, [vp, i64, i64, vp, vp]),
+                "slsp_tiled_meta_bytes": (i64, [i64, i64]),
             }
             for name, (res, args) in sigs.items():
                 fn = getattr(L, name)
@@ -206,7 +208,9 @@ def compress(slided: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
 
 @dataclass
 class PackedWeights:
-    """MMA-ready compressed weights: values n x kp/2, meta n x kp/8 (2-bit codes)."""
+    """MMA-ready compressed weights: values n x kp/2, meta n x kp/8 (row-major
+    2-bit codes, the interchange format) and meta_tiled (slsp_tile_meta, the
+    GEMM operand; built on first use if absent)."""
     values: torch.Tensor
     meta: torch.Tensor
     n: int
@@ -214,10 +218,24 @@ class PackedWeights:
     kp: int
     z: int
     l: int
+    meta_tiled: torch.Tensor | None = None
 
     @property
     def dtype(self) -> int:
         return dtype_code(self.values)
+
+    def tiled(self) -> torch.Tensor:
+        if self.meta_tiled is None:
+            self.meta_tiled = tile_meta(self.meta, self.n, self.kp)
+        return self.meta_tiled
+
+
+def tile_meta(meta: torch.Tensor, rows: int, kp: int) -> torch.Tensor:
+    """Row-major codes -> the MMA-tiled metadata layout (slsp_tile_meta)."""
+    _require_cuda(meta)
+    out = torch.empty(int(lib().slsp_tiled_meta_bytes(rows, kp)), dtype=torch.uint8, device=meta.device)
+    _check(lib().slsp_tile_meta(_ptr(meta), rows, kp, _ptr(out), _stream(meta.device)), "tile_meta")
+    return out
 
 
 def pack_compress(w: torch.Tensor, z: int, l: int, kp: int | None = None, check: bool = True) -> PackedWeights:
@@ -234,7 +252,10 @@ def pack_compress(w: torch.Tensor, z: int, l: int, kp: int | None = None, check:
                                   _ptr(meta), _ptr(ws), C.byref(er), C.byref(eb), _stream(w.device))
     _check(st, "pack_compress", f"row {er.value}, block {eb.value} violates pattern {z}:{l}"
            if st == ERR_NOT_COMPLIANT else None)
-    return PackedWeights(values, meta, rows, cols, kp, z, l)
+    pw = PackedWeights(values, meta, rows, cols, kp, z, l)
+    if kp % 256 == 0:  # GEMM-ready: tile the metadata once, offline
+        pw.tiled()
+    return pw
 
 
 def magnitude_prune(w: torch.Tensor, z: int, l: int) -> torch.Tensor:
@@ -329,7 +350,7 @@ def sparse_gemm(w: PackedWeights, act: torch.Tensor, s_ch: torch.Tensor | None =
         raise DimensionMismatchError("lifted activation width does not match compressed weights")
     o = _gemm_out(out_mode, w.n, m, w.values.dtype == torch.int8, act.device, out)
     ldo = o.shape[1]
-    _check(lib().slsp_sparse_gemm(w.dtype, _ptr(_raw(w.values)), _ptr(w.meta), w.n, w.kp, _ptr(act), m, _ptr(s_ch),
+    _check(lib().slsp_sparse_gemm(w.dtype, _ptr(_raw(w.values)), _ptr(w.tiled()), w.n, w.kp, _ptr(act), m, _ptr(s_ch),
                                   _ptr(s_tok), out_mode, _ptr(o), ldo, _stream(act.device)), "sparse_gemm")
     return o
 

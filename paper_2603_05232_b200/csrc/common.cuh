@@ -119,6 +119,40 @@ SLSP_DEVINL void tma_load_3d_cg2(void* dst, const CUtensorMap* map, uint32_t bar
       : "memory");
 }
 
+// Same, with an L2 eviction-priority policy (createpolicy).
+SLSP_DEVINL void tma_load_2d_cg2_hint(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int c0, int c1,
+                                      uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
+}
+
+// cta_group::2 load multicast to the CTAs in `mask` (same smem offset in each);
+// completion bytes go to each destination pair's leader barrier.
+SLSP_DEVINL void tma_load_2d_cg2_mc(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int c0, int c1,
+                                    uint16_t mask, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5, %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1), "h"(mask), "l"(policy)
+      : "memory");
+}
+
+SLSP_DEVINL void tma_store_2d_hint(const CUtensorMap* map, const void* src, int c0, int c1, uint64_t policy) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "l"(policy)
+               : "memory");
+}
+
+SLSP_DEVINL uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
 // smem -> global tensor store (bulk async group), used by the GEMM epilogue.
 SLSP_DEVINL void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(

@@ -34,15 +34,24 @@ constexpr int kNumThreads = 192;
 // Debug knobs (env SLSP_GEMM_DEBUG, read once): bit0 skip output stores,
 // bit1 skip operand loads (MMA on stale smem), bit2 load k-block 0 of tile 0
 // only (L2-resident operands). Results are garbage when set; perf probing only.
-enum : uint32_t { kDbgNoStore = 1u, kDbgNoLoad = 2u, kDbgSameTile = 4u };
+enum : uint32_t { kDbgNoStore = 1u, kDbgNoLoad = 2u, kDbgSameTile = 4u, kDbgNoMeta = 8u };
+// L2 cache-policy hints (env SLSP_GEMM_HINTS overrides kDefaultHints).
+enum : uint32_t { kHintBLast = 1u, kHintAFirst = 2u, kHintOutFirst = 4u };
+constexpr uint32_t kDefaultHints = kHintBLast | kHintOutFirst;
 
-template <bool SPARSE_, MmaKind KIND_, int BN_, int STAGES_, int OUT_>
+template <bool SPARSE_, MmaKind KIND_, int BN_, int STAGES_, int OUT_, int CL_ = 2>
 struct Cfg {
   static constexpr bool SPARSE = SPARSE_;
   static constexpr MmaKind KIND = KIND_;
   static constexpr int BN = BN_;          // tokens per pair tile (MMA N)
   static constexpr int STAGES = STAGES_;
   static constexpr int OUT = OUT_;
+  // Cluster: CL CTAs = CL/2 CTA pairs on adjacent weight tiles of the same
+  // token tile; with 2 pairs each activation (B) box is fetched once from L2
+  // and multicast to both pairs (each pair loads one half of every B box).
+  static constexpr int CL = CL_;
+  static constexpr int NPAIR = CL / 2;
+  static_assert(CL == 2 || CL == 4, "cluster of 1 or 2 CTA pairs");
   static constexpr int BM = 256;          // weight rows per pair tile (MMA M)
   static constexpr int A_ROWS = 128;      // per CTA
   static constexpr int B_ROWS = BN / 2;   // tokens per CTA
@@ -50,6 +59,8 @@ struct Cfg {
   static constexpr int B_ATOMS = SPARSE ? 2 : 1;             // B bytes per stage = 2x A bytes for .sp
   static constexpr int B_ATOM = B_ROWS * 128;
   static constexpr int B_STAGE = B_ATOM * B_ATOMS;
+  static constexpr int B_PART = B_ROWS / NPAIR;  // rows of each B box one pair fetches (multicast)
+  static_assert(B_PART % 8 == 0, "multicast slices must be whole 128B-swizzle atoms");
   static constexpr int E_STAGE = SPARSE ? 2 * 128 * 16 : 0;  // two 128x128b metadata atoms
   static constexpr int STAGE_TX = A_STAGE + B_STAGE + E_STAGE;
   static constexpr int K_BYTES_B = 128 * B_ATOMS;            // activation bytes consumed per stage
@@ -89,14 +100,18 @@ struct Params {
   int64_t ldo;
   int tma_store;      // 1: swizzled smem staging + TMA store; 0: direct stores
   uint32_t debug;
+  uint32_t hints;     // kHint* L2 policies
+  int group;          // weight tiles per raster band
 };
 
-SLSP_DEVINL void tile_coords(int tile, int m_tiles, int n_tiles, int& mt, int& nt) {
-  constexpr int kGroup = 8;  // weight tiles per raster band (B reuse through L2)
-  const int per_group = kGroup * n_tiles;
+// Raster: bands of `group` weight tiles; within a band the weight tile varies
+// fastest, so the clusters running concurrently share activation tiles (B)
+// and each band's weight tiles stay L2-resident while the band sweeps tokens.
+SLSP_DEVINL void tile_coords(int tile, const Params& p, int m_count, int& mt, int& nt) {
+  const int per_group = p.group * p.n_tiles;
   const int g = tile / per_group;
-  const int first = g * kGroup;
-  const int gsize = min(kGroup, m_tiles - first);
+  const int first = g * p.group;
+  const int gsize = min(p.group, m_count - first);
   const int r = tile - g * per_group;
   mt = first + r % gsize;
   nt = r / gsize;
@@ -166,10 +181,11 @@ SLSP_DEVINL void epilogue_chunk(const Params& p, const CUtensorMap* tmOut, uint8
     fence_async_smem();
     __syncwarp();
     if (lane == 0) {
+      const uint64_t pol = (p.hints & kHintOutFirst) ? policy_evict_first() : policy_evict_normal();
       if constexpr (C::OUT == SLSP_OUT_BF16_MN)
-        tma_store_2d(tmOut, stage, static_cast<int>(row0), static_cast<int>(t0));
+        tma_store_2d_hint(tmOut, stage, static_cast<int>(row0), static_cast<int>(t0), pol);
       else
-        tma_store_2d(tmOut, stage, static_cast<int>(t0), static_cast<int>(row0));
+        tma_store_2d_hint(tmOut, stage, static_cast<int>(t0), static_cast<int>(row0), pol);
       bulk_commit();
     }
     return;
@@ -196,7 +212,7 @@ SLSP_DEVINL void epilogue_chunk(const Params& p, const CUtensorMap* tmOut, uint8
 }
 
 template <typename C>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
+__global__ void __launch_bounds__(kNumThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmE, const __grid_constant__ CUtensorMap tmOut,
                 const Params p) {
@@ -213,16 +229,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const uint32_t warp = threadIdx.x >> 5;
-  const uint32_t rank = cluster_ctarank();
+  const uint32_t crank = cluster_ctarank();     // rank in the cluster
+  const uint32_t pair = crank >> 1;             // CTA pair within the cluster
+  const uint32_t rank = crank & 1;              // rank within the pair (cta_group::2 peer)
+  const uint32_t lead = crank & ~1u;            // cluster rank of this pair's leader
   const bool leader = rank == 0;
-  const int cluster_id = blockIdx.x >> 1;
-  const int num_clusters = gridDim.x >> 1;
-  const int num_tiles = p.m_tiles * p.n_tiles;
+  const int cluster_id = blockIdx.x / C::CL;
+  const int num_clusters = gridDim.x / C::CL;
+  const int m_super = (p.m_tiles + C::NPAIR - 1) / C::NPAIR;  // weight tiles per cluster step
+  const int num_tiles = m_super * p.n_tiles;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], C::NPAIR);  // every pair's MMA must be done with a stage (multicast B)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -249,9 +269,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
       uint32_t phase = 0;
       const bool no_load = p.debug & kDbgNoLoad;
       const bool same = p.debug & kDbgSameTile;
+      // L2 policy: activations (B) are re-read by every weight tile -> keep
+      // them (evict_last); weights stream through a raster band.
+      const uint64_t pol_b = (p.hints & kHintBLast) ? policy_evict_last() : policy_evict_normal();
+      const uint64_t pol_a = (p.hints & kHintAFirst) ? policy_evict_first() : policy_evict_normal();
       for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
-        int mt, nt;
-        tile_coords(tile, p.m_tiles, p.n_tiles, mt, nt);
+        int ms, nt;
+        tile_coords(tile, p, m_super, ms, nt);
+        int mt = ms * C::NPAIR + static_cast<int>(pair);
         if (same) mt = nt = 0;
         const int a_row = mt * C::BM + static_cast<int>(rank) * C::A_ROWS;
         const int b_row = nt * C::BN + static_cast<int>(rank) * C::B_ROWS;
@@ -261,14 +286,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
           if (no_load) {
             if (leader) mbar_arrive(&full[stage]);
           } else {
-            if (leader) mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_TX);
-            const uint32_t bar = mapa_shared(smem_u32(&full[stage]), 0);
-            tma_load_2d_cg2(sA + stage * C::A_STAGE, &tmA, bar, kl * 128, a_row);
+            const bool skip_e = p.debug & kDbgNoMeta;
+            if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (C::STAGE_TX - (skip_e ? C::E_STAGE : 0)));
+            const uint32_t bar = mapa_shared(smem_u32(&full[stage]), lead);
+            tma_load_2d_cg2_hint(sA + stage * C::A_STAGE, &tmA, bar, kl * 128, a_row, pol_a);
 #pragma unroll
-            for (int at = 0; at < C::B_ATOMS; ++at)
-              tma_load_2d_cg2(sB + stage * C::B_STAGE + at * C::B_ATOM, &tmB, bar, kl * C::K_BYTES_B + at * 128,
-                              b_row);
-            if constexpr (C::SPARSE) tma_load_3d_cg2(sE + stage * C::E_STAGE, &tmE, bar, 0, a_row, kl * 2);
+            for (int at = 0; at < C::B_ATOMS; ++at) {
+              uint8_t* dst = sB + stage * C::B_STAGE + at * C::B_ATOM;
+              if constexpr (C::NPAIR == 1) {
+                tma_load_2d_cg2_hint(dst, &tmB, bar, kl * C::K_BYTES_B + at * 128, b_row, pol_b);
+              } else {  // this pair fetches slice `pair` of the box for the same-rank CTA of every pair
+                const uint16_t mask = static_cast<uint16_t>((1u << rank) | (1u << (rank + 2)));
+                tma_load_2d_cg2_mc(dst + pair * C::B_PART * 128, &tmB, bar, kl * C::K_BYTES_B + at * 128,
+                                   b_row + static_cast<int>(pair) * C::B_PART, mask, pol_b);
+              }
+            }
+            if constexpr (C::SPARSE)  // one contiguous 4 KB tiled-metadata block per stage
+              if (!skip_e)
+                tma_load_2d_cg2_hint(sE + stage * C::E_STAGE, &tmE, bar, 0, ((a_row >> 7) * p.num_kb + kl) * 16,
+                                     pol_a);
           }
           if (++stage == C::STAGES) {
             stage = 0;
@@ -312,13 +348,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
               umma_dense_cg2<C::KIND>(d_tmem, adesc, bdesc, C::IDESC, acc_flag);
             }
           }
-          tc_commit_mc(&empty[stage], 0x3);
+          tc_commit_mc(&empty[stage], static_cast<uint16_t>((1u << C::CL) - 1));  // every CTA of the cluster
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc_commit_mc(&tfull[acc], 0x3);
+        tc_commit_mc(&tfull[acc], static_cast<uint16_t>(0x3u << lead));  // this pair's epilogues
       }
     }
   } else {
@@ -329,8 +365,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
     int buf = 0;
     int it = 0;
     for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
-      int mt, nt;
-      tile_coords(tile, p.m_tiles, p.n_tiles, mt, nt);
+      int ms, nt;
+      tile_coords(tile, p, m_super, ms, nt);
+      const int mt = ms * C::NPAIR + static_cast<int>(pair);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(&tfull[acc], acc_phase);
@@ -355,7 +392,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+      if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), lead));
     }
     if (lane == 0) bulk_wait<0>();
   }
@@ -393,6 +430,12 @@ uint32_t debug_flags() {
   return flags;
 }
 
+// Tuning knob from the environment (read per call: cheap, and lets probes vary it).
+uint32_t env_knob(const char* name, uint32_t dflt) {
+  const char* e = std::getenv(name);
+  return e ? static_cast<uint32_t>(std::strtoul(e, nullptr, 0)) : dflt;
+}
+
 // Byte-addressed 2D map (uint8 elements): rows x row_bytes, box rows x 128 B, 128B swizzle.
 int make_map_2d(CUtensorMap* map, const void* base, uint64_t row_bytes, uint64_t rows, uint32_t box_rows) {
   EncodeTiledFn enc = get_encode();
@@ -407,16 +450,19 @@ int make_map_2d(CUtensorMap* map, const void* base, uint64_t row_bytes, uint64_t
   return r == CUDA_SUCCESS ? SLSP_OK : SLSP_ERR_CUDA;
 }
 
-// Metadata map: meta is rows x (kp/8) bytes. Viewed as (16 B, rows, kp/128)
-// so one box {16, 128, 2} lands as two canonical 128x16B UTCCP atoms.
+// Metadata map over the slsp_tile_meta layout: a flat byte stream viewed as
+// 256-byte rows; one box {256, 16} is the contiguous 4 KB block of a stage
+// (two canonical 128x16B tcgen05.cp atoms) — 16 wide requests instead of 256
+// 16-byte ones.
 int make_map_meta(CUtensorMap* map, const void* base, uint64_t rows, uint64_t kp) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return SLSP_ERR_CUDA;
-  cuuint64_t dims[3] = {16, rows, kp / 128};
-  cuuint64_t strides[2] = {kp / 8, 16};
-  cuuint32_t box[3] = {16, 128, 2};
-  cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, estr,
+  const uint64_t bytes = static_cast<uint64_t>(slsp_tiled_meta_bytes(static_cast<int64_t>(rows), static_cast<int64_t>(kp)));
+  cuuint64_t dims[2] = {256, bytes / 256};
+  cuuint64_t strides[1] = {256};
+  cuuint32_t box[2] = {256, 16};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? SLSP_OK : SLSP_ERR_CUDA;
@@ -458,43 +504,66 @@ int num_sms() {
 template <typename C>
 int run(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const CUtensorMap& o, Params p,
         cudaStream_t s) {
-  static bool configured = false;
+  static int max_clusters = 0;
   auto kern = gemm_kernel<C>;
-  if (!configured) {
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C::CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(kNumThreads);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (!max_clusters) {  // how many clusters of this shape are co-resident (GPC packing)
     SLSP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    configured = true;
+    cfg.gridDim = dim3(C::CL * (num_sms() / C::CL));
+    int n = 0;
+    SLSP_CUDA_TRY(cudaOccupancyMaxActiveClusters(&n, kern, &cfg));
+    max_clusters = n > 0 ? n : num_sms() / C::CL;
   }
   p.m_tiles = static_cast<int>((p.n + C::BM - 1) / C::BM);
   p.n_tiles = static_cast<int>((p.m + C::BN - 1) / C::BN);
-  const int tiles = p.m_tiles * p.n_tiles;
+  const int tiles = (p.m_tiles + C::NPAIR - 1) / C::NPAIR * p.n_tiles;
   if (tiles == 0) return SLSP_OK;
-  int clusters = num_sms() / 2;
-  static const int cluster_cap = [] {
-    const char* e = std::getenv("SLSP_GEMM_CLUSTERS");  // perf probing: cap the persistent grid
-    return e ? std::atoi(e) : 0;
-  }();
+  int clusters = max_clusters;
+  const int cluster_cap = static_cast<int>(env_knob("SLSP_GEMM_CLUSTERS", 0));  // perf probing
   if (cluster_cap > 0 && clusters > cluster_cap) clusters = cluster_cap;
   if (clusters > tiles) clusters = tiles;
-  kern<<<2 * clusters, kNumThreads, C::SMEM, s>>>(a, b, e, o, p);
-  SLSP_LAUNCH_CHECK();
+  cfg.gridDim = dim3(C::CL * clusters);
+  SLSP_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, a, b, e, o, p));
   return SLSP_OK;
 }
 
-template <bool SPARSE, MmaKind K, int BN, int ST>
-int run_out(int out_mode, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const CUtensorMap& o,
-            const Params& p, cudaStream_t s) {
+template <bool SPARSE, MmaKind K, int BN, int ST, int CL>
+int run_out_cl(int out_mode, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const CUtensorMap& o,
+               const Params& p, cudaStream_t s) {
   switch (out_mode) {
-    case SLSP_OUT_RAW_NM: return run<Cfg<SPARSE, K, BN, ST, SLSP_OUT_RAW_NM>>(a, b, e, o, p, s);
-    case SLSP_OUT_BF16_NM: return run<Cfg<SPARSE, K, BN, ST, SLSP_OUT_BF16_NM>>(a, b, e, o, p, s);
-    case SLSP_OUT_BF16_MN: return run<Cfg<SPARSE, K, BN, ST, SLSP_OUT_BF16_MN>>(a, b, e, o, p, s);
+    case SLSP_OUT_RAW_NM: return run<Cfg<SPARSE, K, BN, ST, SLSP_OUT_RAW_NM, CL>>(a, b, e, o, p, s);
+    case SLSP_OUT_BF16_NM: return run<Cfg<SPARSE, K, BN, ST, SLSP_OUT_BF16_NM, CL>>(a, b, e, o, p, s);
+    case SLSP_OUT_BF16_MN: return run<Cfg<SPARSE, K, BN, ST, SLSP_OUT_BF16_MN, CL>>(a, b, e, o, p, s);
   }
   return SLSP_ERR_INVALID;
+}
+
+// Cluster shape: 2 (one CTA pair) or 4 (two pairs sharing activation tiles by
+// TMA multicast); env SLSP_GEMM_CLUSTER overrides the per-kernel default.
+template <bool SPARSE, MmaKind K, int BN, int ST>
+int run_out(int out_mode, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const CUtensorMap& o,
+            const Params& p, cudaStream_t s, uint32_t default_cluster) {
+  if (env_knob("SLSP_GEMM_CLUSTER", default_cluster) == 4)
+    return run_out_cl<SPARSE, K, BN, ST, 4>(out_mode, a, b, e, o, p, s);
+  return run_out_cl<SPARSE, K, BN, ST, 2>(out_mode, a, b, e, o, p, s);
 }
 
 constexpr int kSparseBN = 224;
 constexpr int kSparseStages = 4;
 constexpr int kDenseBN = 256;
 constexpr int kDenseStages = 6;
+constexpr uint32_t kSparseCluster = 2;
+constexpr uint32_t kDenseCluster = 2;
 
 int check_out(int out_mode, const float* s_ch, const float* s_tok, void* out, int64_t ldo, int64_t n, int64_t m) {
   if (!out) return SLSP_ERR_INVALID;
@@ -541,9 +610,11 @@ int slsp_sparse_gemm(int dtype, const void* values, const uint8_t* meta, int64_t
   p.out = out;
   p.ldo = ldo;
   p.debug = debug_flags();
+  p.hints = env_knob("SLSP_GEMM_HINTS", kDefaultHints);
+  p.group = static_cast<int>(env_knob("SLSP_GEMM_GROUP", 8));
   if (dtype == SLSP_DT_I8)
-    return run_out<true, MmaKind::I8, kSparseBN, kSparseStages>(out_mode, ta, tb, te, to, p, s);
-  return run_out<true, MmaKind::F8, kSparseBN, kSparseStages>(out_mode, ta, tb, te, to, p, s);
+    return run_out<true, MmaKind::I8, kSparseBN, kSparseStages>(out_mode, ta, tb, te, to, p, s, kSparseCluster);
+  return run_out<true, MmaKind::F8, kSparseBN, kSparseStages>(out_mode, ta, tb, te, to, p, s, kSparseCluster);
 }
 
 int slsp_dense_gemm(int dtype, const void* w, int64_t n, int64_t k, const void* act, int64_t m, const float* s_ch,
@@ -573,11 +644,13 @@ int slsp_dense_gemm(int dtype, const void* w, int64_t n, int64_t k, const void* 
   p.out = out;
   p.ldo = ldo;
   p.debug = debug_flags();
+  p.hints = env_knob("SLSP_GEMM_HINTS", kDefaultHints);
+  p.group = static_cast<int>(env_knob("SLSP_GEMM_GROUP", 8));
   if (dtype == SLSP_DT_I8)
-    return run_out<false, MmaKind::I8, kDenseBN, kDenseStages>(out_mode, ta, tb, ta, to, p, s);
+    return run_out<false, MmaKind::I8, kDenseBN, kDenseStages>(out_mode, ta, tb, ta, to, p, s, kDenseCluster);
   if (dtype == SLSP_DT_E4M3)
-    return run_out<false, MmaKind::F8, kDenseBN, kDenseStages>(out_mode, ta, tb, ta, to, p, s);
-  return run_out<false, MmaKind::F16, kDenseBN, kDenseStages>(out_mode, ta, tb, ta, to, p, s);
+    return run_out<false, MmaKind::F8, kDenseBN, kDenseStages>(out_mode, ta, tb, ta, to, p, s, kDenseCluster);
+  return run_out<false, MmaKind::F16, kDenseBN, kDenseStages>(out_mode, ta, tb, ta, to, p, s, kDenseCluster);
 }
 
 }  // extern "C"

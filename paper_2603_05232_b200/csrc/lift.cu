@@ -174,8 +174,175 @@ __global__ void __launch_bounds__(kThreads) act_kernel(ActArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fast path: one WARP per token row, no shared memory. A lane owns "quads" of
+// 4 consecutive source blocks (4*L elements, a whole number of 16-byte
+// vectors for every (2N-2):2N pattern), so every lifted window of a quad is
+// built from registers: window w of block g covers bytes [g*L + 2w, +4) of
+// the quad's codes. Pass 1 streams the row for |x|max (vector loads, warp
+// shuffle reduce); pass 2 re-reads it (L1/L2-resident), quantizes each source
+// element once in double and emits the quad's lifted words as 16-byte stores.
+// Requirements (host-checked): cols % (4*L) == 0, 16-byte aligned rows.
+template <int IN, int KIND, int L>
+struct WarpGeom {
+  static constexpr int ESZ = IN == IN_F32 ? 4 : 2;
+  static constexpr int WC = (L - 4) / 2 + 1;
+  static constexpr int ELEMS = 4 * L;               // source elements per quad
+  static constexpr int IN_VEC = ELEMS * ESZ / 16;   // 16-byte loads per quad
+  static constexpr int OUT_ELEMS = 4 * WC * 4;      // lifted elements per quad
+  static constexpr int OESZ = KIND == K_NONE ? ESZ : 1;
+  static constexpr int OUT_VEC = OUT_ELEMS * OESZ / 16;
+  static_assert(ELEMS * ESZ % 16 == 0 && OUT_ELEMS * OESZ % 16 == 0, "quad must be whole vectors");
+};
+
+template <int IN, int N>
+SLSP_DEVINL float elem(const uint4 (&v)[N], int e) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(v);
+  if constexpr (IN == IN_F32) return __uint_as_float(w[e]);
+  return __uint_as_float(((w[e >> 1] >> (16 * (e & 1))) & 0xFFFFu) << 16);
+}
+
+template <int IN, int KIND, int L>
+__global__ void __launch_bounds__(256) act_warp_kernel(ActArgs a) {
+  using G = WarpGeom<IN, KIND, L>;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int nquads = static_cast<int>(a.cols / G::ELEMS);
+  const int out_vecs = static_cast<int>(a.out_bytes >> 4);
+  for (int64_t row = warp0; row < a.rows; row += nwarps) {
+    const uint4* src = reinterpret_cast<const uint4*>(a.x + row * a.cols * G::ESZ);
+    uint4* dst = reinterpret_cast<uint4*>(a.out + row * a.out_bytes);
+    double r = 0.0;
+    if constexpr (KIND != K_NONE) {
+      float amax = 0.f;
+      int bad = 0;
+#pragma unroll 2
+      for (int q = lane; q < nquads; q += 32) {
+        uint4 v[G::IN_VEC];
+#pragma unroll
+        for (int i = 0; i < G::IN_VEC; ++i) v[i] = __ldg(src + q * G::IN_VEC + i);
+#pragma unroll
+        for (int e = 0; e < G::ELEMS; ++e) {
+          const float f = elem<IN>(v, e);
+          bad |= !isfinite(f);
+          amax = fmaxf(amax, fabsf(f));
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+        bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+      }
+      if (bad && lane == 0 && a.status) atomicMin(a.status, static_cast<unsigned long long>(row) << 32);
+      // quantize.hpp:151-153, in double
+      const double qmax = KIND == K_INT8 ? 127.0 : 448.0;
+      const double absmax = static_cast<double>(amax);
+      r = absmax == 0.0 ? 0.0 : qmax / absmax;
+      if (lane == 0) a.scales[row] = absmax == 0.0 ? 1.0f : __double2float_rn(absmax / qmax);
+    }
+#pragma unroll 2
+    for (int q = lane; q < nquads; q += 32) {
+      uint4 v[G::IN_VEC];
+#pragma unroll
+      for (int i = 0; i < G::IN_VEC; ++i) v[i] = __ldg(src + q * G::IN_VEC + i);
+      uint32_t o[G::OUT_VEC * 4];
+      if constexpr (KIND != K_NONE) {
+        uint32_t qw[G::ELEMS / 4 + 1];
+#pragma unroll
+        for (int i = 0; i < G::ELEMS / 4 + 1; ++i) qw[i] = 0;
+#pragma unroll
+        for (int e = 0; e < G::ELEMS; ++e)
+          qw[e >> 2] |= static_cast<uint32_t>(quantize_value(static_cast<double>(elem<IN>(v, e)) * r, KIND))
+                        << (8 * (e & 3));
+#pragma unroll
+        for (int g = 0; g < 4; ++g)
+#pragma unroll
+          for (int w = 0; w < G::WC; ++w) {
+            const int b = g * L + 2 * w;  // even byte offset of the window in the quad
+            o[g * G::WC + w] = (b & 3) ? __byte_perm(qw[b >> 2], qw[(b >> 2) + 1], 0x5432) : qw[b >> 2];
+          }
+      } else {  // passthrough lift of raw elements
+        const uint32_t* iw = reinterpret_cast<const uint32_t*>(v);
+#pragma unroll
+        for (int g = 0; g < 4; ++g)
+#pragma unroll
+          for (int w = 0; w < G::WC; ++w) {
+            const int b = g * L + 2 * w;  // element offset
+            if constexpr (G::ESZ == 2) {
+              o[(g * G::WC + w) * 2] = iw[b >> 1];
+              o[(g * G::WC + w) * 2 + 1] = iw[(b >> 1) + 1];
+            } else {
+#pragma unroll
+              for (int d = 0; d < 4; ++d) o[(g * G::WC + w) * 4 + d] = iw[b + d];
+            }
+          }
+      }
+#pragma unroll
+      for (int i = 0; i < G::OUT_VEC; ++i)
+        dst[q * G::OUT_VEC + i] = make_uint4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
+    }
+    for (int i = nquads * G::OUT_VEC + lane; i < out_vecs; i += 32) dst[i] = make_uint4(0, 0, 0, 0);  // kp padding
+  }
+}
+
+template <int IN, int KIND, int L>
+int launch_warp(ActArgs& a, cudaStream_t s) {
+  static int grid_cap = 0;
+  auto k = act_warp_kernel<IN, KIND, L>;
+  if (!grid_cap) {
+    int dev = 0, sms = 0, per_sm = 0;
+    SLSP_CUDA_TRY(cudaGetDevice(&dev));
+    SLSP_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    SLSP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, 0));
+    grid_cap = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  const int64_t blocks = (a.rows + 7) / 8;
+  k<<<static_cast<unsigned>(blocks < grid_cap ? blocks : grid_cap), 256, 0, s>>>(a);
+  SLSP_LAUNCH_CHECK();
+  return SLSP_OK;
+}
+
+// Returns 1 and launches when the warp fast path applies, 0 to fall back.
+template <int IN, int KIND>
+int try_warp_path(ActArgs& a, cudaStream_t s, int* st) {
+  const int esz = IN == IN_F32 ? 4 : 2;
+  const int oesz = KIND == K_NONE ? esz : 1;
+  if (a.rows == 0) return 0;
+  if ((reinterpret_cast<uintptr_t>(a.x) & 15u) || (reinterpret_cast<uintptr_t>(a.out) & 15u)) return 0;
+  if (a.cols % (4 * a.l) != 0 || (a.cols * esz) % 16 != 0 || a.out_bytes % 16 != 0) return 0;
+  if (a.words_real * 4 * oesz > a.out_bytes) return 0;
+  switch (a.l) {
+    case 6: *st = launch_warp<IN, KIND, 6>(a, s); return 1;
+    case 8: *st = launch_warp<IN, KIND, 8>(a, s); return 1;
+    case 10: *st = launch_warp<IN, KIND, 10>(a, s); return 1;
+    case 16: *st = launch_warp<IN, KIND, 16>(a, s); return 1;
+    default: return 0;
+  }
+}
+
+// quantize_rows on the warp path: the 2:4 "identity" geometry (L = 4, one
+// window per block at offset 0) maps every source byte to itself.
+template <int IN, int KIND>
+int try_warp_identity(ActArgs& a, cudaStream_t s, int* st) {
+  const int esz = IN == IN_F32 ? 4 : 2;
+  if (a.rows == 0) return 0;
+  if ((reinterpret_cast<uintptr_t>(a.x) & 15u) || (reinterpret_cast<uintptr_t>(a.out) & 15u)) return 0;
+  if (a.cols % 16 != 0 || (a.cols * esz) % 16 != 0 || a.out_bytes % 16 != 0) return 0;
+  *st = launch_warp<IN, KIND, 4>(a, s);
+  return 1;
+}
+
 template <int IN, int KIND, bool LIFT>
 int launch_act(ActArgs& a, int esz, cudaStream_t s) {
+  {
+    int st = SLSP_OK;
+    if constexpr (LIFT) {
+      if (try_warp_path<IN, KIND>(a, s, &st)) return st;
+    } else if constexpr (KIND != K_NONE) {
+      if (try_warp_identity<IN, KIND>(a, s, &st)) return st;
+    }
+  }
   if (a.rows == 0) return SLSP_OK;
   const size_t smem = ((a.in_cols_pad * esz + 15) & ~static_cast<int64_t>(15)) + (KIND != K_NONE ? a.in_cols_pad : 0);
   if (smem > 200 * 1024) return SLSP_ERR_UNSUPPORTED;

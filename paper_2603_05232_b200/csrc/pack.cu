@@ -235,6 +235,25 @@ __global__ void prune_kernel(const uint8_t* w, int64_t rows, int64_t cols, int z
   }
 }
 
+// Row-major 2-bit codes -> MMA-tiled metadata (see slsp_tile_meta in the
+// header): one 16-byte chunk per thread, coalesced on the tiled side.
+__global__ void tile_meta_kernel(const uint8_t* __restrict__ meta, int64_t rows, int64_t kp, uint8_t* tiled) {
+  const int64_t ld = kp / 8;
+  const int64_t stages = kp / 256;
+  const int64_t total = (rows + 127) / 128 * 128 * ld / 16;  // 16-byte chunks
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i & 127;        // row within the 128-row block
+    const int64_t c = (i >> 7) & 1;   // atom within the stage
+    const int64_t bs = i >> 8;        // b * stages + s
+    const int64_t b = bs / stages, s = bs % stages;
+    const int64_t row = b * 128 + r;
+    uint4 v = make_uint4(0x44444444u, 0x44444444u, 0x44444444u, 0x44444444u);
+    if (row < rows) v = *reinterpret_cast<const uint4*>(meta + row * ld + s * 32 + c * 16);
+    reinterpret_cast<uint4*>(tiled)[i] = v;
+  }
+}
+
 template <int MODE>
 int launch_pack(int esz, PackArgs& a, cudaStream_t s) {
   const int64_t chunks = (a.group_slots + kThreads - 1) / kThreads;
@@ -339,6 +358,23 @@ int slsp_pack_compress(int dtype, const void* w, int64_t rows, int64_t cols, int
   a.status = status;
   if ((st = launch_pack<1>(esz, a, s))) return st;
   return status_collect(status_ws, s, SLSP_ERR_NOT_COMPLIANT, err_row, err_block);
+}
+
+int64_t slsp_tiled_meta_bytes(int64_t rows, int64_t kp) { return (rows + 127) / 128 * 128 * (kp / 8); }
+
+int slsp_tile_meta(const uint8_t* meta, int64_t rows, int64_t kp, uint8_t* tiled, slsp_stream_t stream) {
+  using namespace slsp_host;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (rows < 0 || kp <= 0 || !meta || !tiled) return SLSP_ERR_INVALID;
+  if (kp % 256 != 0) return SLSP_ERR_DIMENSION;
+  if ((reinterpret_cast<uintptr_t>(meta) | reinterpret_cast<uintptr_t>(tiled)) & 15u) return SLSP_ERR_INVALID;
+  int st;
+  if ((st = require_sm100())) return st;
+  const int64_t chunks = slsp_tiled_meta_bytes(rows, kp) / 16;
+  if (chunks == 0) return SLSP_OK;
+  tile_meta_kernel<<<grid_for(chunks, 256), 256, 0, s>>>(meta, rows, kp, tiled);
+  SLSP_LAUNCH_CHECK();
+  return SLSP_OK;
 }
 
 int slsp_compress(int dtype, const void* slided, int64_t rows, int64_t cols_exp, void* values, uint8_t* codes,

@@ -1,8 +1,8 @@
 #!/bin/bash
 # Scaling of GEMM throughput with the number of active CTA pairs (per-SM vs shared limit).
 out=${1:-gpurun_out}
-for c in 74 37 18 9; do
-  for dbg in 0 4; do
+for c in ${CLUSTERS:-74 9}; do
+  for dbg in ${DBGS:-0 8}; do
     SLSP_GEMM_CLUSTERS=$c SLSP_GEMM_DEBUG=$dbg timeout 300 python bench.py --steps 3 --warmup 1 --no-e2e --no-cpu > $out/grid_${c}_$dbg.json 2>/dev/null
     python - "$out/grid_${c}_$dbg.json" "$c" "$dbg" <<'PY'
 import json, sys

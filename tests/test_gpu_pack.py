@@ -176,3 +176,17 @@ def test_prune_then_pack_full_shape_roundtrip(slsp):
     meta = pw.meta[:, : kprime // 8].to(torch.int32)
     nib = torch.stack([(meta >> (4 * i)) & 0xF for i in range(2)], dim=-1).reshape(n, -1)
     assert bool(((nib & 3) < (nib >> 2)).all())
+
+
+def test_tile_meta_layout(slsp):
+    """slsp_tile_meta: 4 KB blocks per (128-row block, 256-wide k-stage), two
+    128x16B atoms each; padding rows canonical 0x44 (include/slsp_b200.h)."""
+    rng = np.random.default_rng(12)
+    rows, kp = 300, 768
+    meta = rng.integers(0, 256, size=(rows, kp // 8)).astype(np.uint8)
+    got = slsp.tile_meta(dev(meta), rows, kp).cpu().numpy()
+    nb = -(-rows // 128)
+    padded = np.full((nb * 128, kp // 8), 0x44, np.uint8)
+    padded[:rows] = meta
+    want = padded.reshape(nb, 128, kp // 256, 2, 16).transpose(0, 2, 3, 1, 4).reshape(-1)
+    assert np.array_equal(got, want)
