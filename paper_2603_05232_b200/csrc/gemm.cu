@@ -39,7 +39,7 @@ enum : uint32_t { kDbgNoStore = 1u, kDbgNoLoad = 2u, kDbgSameTile = 4u, kDbgNoMe
 enum : uint32_t { kHintBLast = 1u, kHintAFirst = 2u, kHintOutFirst = 4u };
 constexpr uint32_t kDefaultHints = kHintBLast | kHintOutFirst;
 
-template <bool SPARSE_, MmaKind KIND_, int BN_, int STAGES_, int OUT_, int CL_ = 2>
+template <bool SPARSE_, MmaKind KIND_, int BN_, int STAGES_, int OUT_, int CL_ = 2, int MSUB_ = 1>
 struct Cfg {
   static constexpr bool SPARSE = SPARSE_;
   static constexpr MmaKind KIND = KIND_;
@@ -52,41 +52,52 @@ struct Cfg {
   static constexpr int CL = CL_;
   static constexpr int NPAIR = CL / 2;
   static_assert(CL == 2 || CL == 4, "cluster of 1 or 2 CTA pairs");
-  static constexpr int BM = 256;          // weight rows per pair tile (MMA M)
-  static constexpr int A_ROWS = 128;      // per CTA
+  // M-subtiles: the pair runs MSUB UMMAs (M=256 each) per k-step against the
+  // same activation stage, so B traffic per MAC drops by MSUB. TMEM then holds
+  // MSUB accumulators per tile; with MSUB=2 they are single-buffered and
+  // 4*MSUB epilogue warps drain them in parallel.
+  static constexpr int MSUB = MSUB_;
+  static_assert(MSUB == 1 || MSUB == 2, "one or two M-subtiles per pair");
+  static constexpr int ACC_STAGES = MSUB == 1 ? 2 : 1;
+  static constexpr int EPI_WARPS = 4 * MSUB;
+  static constexpr int THREADS = 64 + 32 * EPI_WARPS;
+  static constexpr int BM = 256 * MSUB;   // weight rows per pair tile
+  static constexpr int A_ROWS = 128;      // per CTA per M-subtile
   static constexpr int B_ROWS = BN / 2;   // tokens per CTA
-  static constexpr int A_STAGE = 128 * 128;                  // one 128B-swizzle atom column
+  static constexpr int A_SUB = 128 * 128;                    // one 128B-swizzle atom column
+  static constexpr int A_STAGE = MSUB * A_SUB;
   static constexpr int B_ATOMS = SPARSE ? 2 : 1;             // B bytes per stage = 2x A bytes for .sp
   static constexpr int B_ATOM = B_ROWS * 128;
   static constexpr int B_STAGE = B_ATOM * B_ATOMS;
   static constexpr int B_PART = B_ROWS / NPAIR;  // rows of each B box one pair fetches (multicast)
   static_assert(B_PART % 8 == 0, "multicast slices must be whole 128B-swizzle atoms");
-  static constexpr int E_STAGE = SPARSE ? 2 * 128 * 16 : 0;  // two 128x128b metadata atoms
+  static constexpr int E_SUB = SPARSE ? 2 * 128 * 16 : 0;    // two 128x128b metadata atoms
+  static constexpr int E_STAGE = MSUB * E_SUB;
   static constexpr int STAGE_TX = A_STAGE + B_STAGE + E_STAGE;
   static constexpr int K_BYTES_B = 128 * B_ATOMS;            // activation bytes consumed per stage
-  static constexpr int MMAS = 4;                             // per stage
+  static constexpr int MMAS = 4;                             // k-steps per stage
   static constexpr int ACC_COLS = BN;                        // 32-bit TMEM columns per accumulator
-  static constexpr int E_COL = 2 * BN;                       // metadata columns after both accumulators
+  static constexpr int E_COL = ACC_STAGES * MSUB * BN;       // metadata columns after the accumulators
   static constexpr int TMEM_COLS = 512;
-  static_assert(!SPARSE || E_COL + 8 <= TMEM_COLS, "TMEM budget: 2 accumulators + metadata");
-  static_assert(SPARSE || 2 * BN <= TMEM_COLS, "TMEM budget: 2 accumulators");
+  static_assert(!SPARSE || E_COL + 8 * MSUB <= TMEM_COLS, "TMEM budget: accumulators + metadata");
+  static_assert(SPARSE || E_COL <= TMEM_COLS, "TMEM budget: accumulators");
   static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "cta_group::2 N");
   // epilogue staging: per warp, EPI_BUFS tiles of 32 rows x 32 columns
   static constexpr int OUT_ESZ = OUT == SLSP_OUT_RAW_NM ? 4 : 2;
-  static constexpr int EPI_BUFS = OUT == SLSP_OUT_RAW_NM ? 1 : 2;
+  static constexpr int EPI_BUFS = (OUT == SLSP_OUT_RAW_NM || MSUB == 2) ? 1 : 2;
   static constexpr int EPI_BUF = 32 * 32 * OUT_ESZ;
   static constexpr int EPI_WARP = EPI_BUFS * EPI_BUF;
   static constexpr int OFF_A = 0;
   static constexpr int OFF_B = OFF_A + STAGES * A_STAGE;
   static constexpr int OFF_E = OFF_B + STAGES * B_STAGE;
   static constexpr int OFF_EPI = OFF_E + STAGES * E_STAGE;
-  static constexpr int OFF_BAR = OFF_EPI + 4 * EPI_WARP;
+  static constexpr int OFF_BAR = OFF_EPI + EPI_WARPS * EPI_WARP;
   static constexpr int NUM_BARS = 2 * STAGES + 4;
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16 + 1024;  // + alignment slack
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
   static constexpr uint32_t C_FMT = KIND == MmaKind::I8 ? 2u : 1u;
   static constexpr uint32_t AB_FMT = KIND == MmaKind::F8 ? 0u : 1u;
-  static constexpr uint32_t IDESC = make_idesc(SPARSE, C_FMT, AB_FMT, AB_FMT, BM, BN);
+  static constexpr uint32_t IDESC = make_idesc(SPARSE, C_FMT, AB_FMT, AB_FMT, 256, BN);
   using Acc = typename std::conditional<KIND == MmaKind::I8, int32_t, float>::type;
 };
 
@@ -212,7 +223,7 @@ SLSP_DEVINL void epilogue_chunk(const Params& p, const CUtensorMap* tmOut, uint8
 }
 
 template <typename C>
-__global__ void __launch_bounds__(kNumThreads, 1)
+__global__ void __launch_bounds__(C::THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmE, const __grid_constant__ CUtensorMap tmOut,
                 const Params p) {
@@ -246,7 +257,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 2 * 4);  // 4 epilogue warps in each CTA of the pair
+      mbar_init(&tempty[a], 2 * C::EPI_WARPS);  // every epilogue warp of both CTAs of the pair
     }
     fence_mbar_init();
   }
@@ -289,7 +300,10 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             const bool skip_e = p.debug & kDbgNoMeta;
             if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (C::STAGE_TX - (skip_e ? C::E_STAGE : 0)));
             const uint32_t bar = mapa_shared(smem_u32(&full[stage]), lead);
-            tma_load_2d_cg2_hint(sA + stage * C::A_STAGE, &tmA, bar, kl * 128, a_row, pol_a);
+#pragma unroll
+            for (int h = 0; h < C::MSUB; ++h)
+              tma_load_2d_cg2_hint(sA + stage * C::A_STAGE + h * C::A_SUB, &tmA, bar, kl * 128, a_row + h * 256,
+                                   pol_a);
 #pragma unroll
             for (int at = 0; at < C::B_ATOMS; ++at) {
               uint8_t* dst = sB + stage * C::B_STAGE + at * C::B_ATOM;
@@ -301,10 +315,12 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                                    b_row + static_cast<int>(pair) * C::B_PART, mask, pol_b);
               }
             }
-            if constexpr (C::SPARSE)  // one contiguous 4 KB tiled-metadata block per stage
+            if constexpr (C::SPARSE)  // one contiguous 4 KB tiled-metadata block per stage and subtile
               if (!skip_e)
-                tma_load_2d_cg2_hint(sE + stage * C::E_STAGE, &tmE, bar, 0, ((a_row >> 7) * p.num_kb + kl) * 16,
-                                     pol_a);
+#pragma unroll
+                for (int h = 0; h < C::MSUB; ++h)
+                  tma_load_2d_cg2_hint(sE + stage * C::E_STAGE + h * C::E_SUB, &tmE, bar, 0,
+                                       (((a_row + h * 256) >> 7) * p.num_kb + kl) * 16, pol_a);
           }
           if (++stage == C::STAGES) {
             stage = 0;
@@ -320,11 +336,11 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       uint32_t phase = 0;
       int it = 0;
       for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
-        const int acc = it & 1;
-        const uint32_t acc_phase = (it >> 1) & 1;
+        const int acc = C::ACC_STAGES == 2 ? (it & 1) : 0;
+        const uint32_t acc_phase = C::ACC_STAGES == 2 ? ((it >> 1) & 1) : (it & 1);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem + acc * C::ACC_COLS;
+        const uint32_t d_tmem = tmem + acc * C::MSUB * C::ACC_COLS;
         for (int kb = 0; kb < p.num_kb; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -333,19 +349,26 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           if constexpr (C::SPARSE) {
             const uint32_t e_base = smem_u32(sE + stage * C::E_STAGE);
 #pragma unroll
-            for (int c = 0; c < 2; ++c)
-              tmem_cp_128x128b_cg2(tmem + C::E_COL + 4 * c, smem_desc(e_base + c * 2048, 2048, 128, 0));
+            for (int h = 0; h < C::MSUB; ++h)
+#pragma unroll
+              for (int c = 0; c < 2; ++c)
+                tmem_cp_128x128b_cg2(tmem + C::E_COL + 8 * h + 4 * c,
+                                     smem_desc(e_base + h * C::E_SUB + c * 2048, 2048, 128, 0));
           }
 #pragma unroll
           for (int j = 0; j < C::MMAS; ++j) {
-            const uint64_t adesc = smem_desc(a_base + j * 32, 16, 1024, 2);
             const uint32_t acc_flag = (kb | j) != 0;
-            if constexpr (C::SPARSE) {
-              const uint64_t bdesc = smem_desc(b_base + (j >> 1) * C::B_ATOM + (j & 1) * 64, 16, 1024, 2);
-              umma_sparse_cg2<C::KIND>(d_tmem, adesc, bdesc, tmem + C::E_COL + 2 * j, C::IDESC, acc_flag);
-            } else {
-              const uint64_t bdesc = smem_desc(b_base + j * 32, 16, 1024, 2);
-              umma_dense_cg2<C::KIND>(d_tmem, adesc, bdesc, C::IDESC, acc_flag);
+#pragma unroll
+            for (int h = 0; h < C::MSUB; ++h) {
+              const uint64_t adesc = smem_desc(a_base + h * C::A_SUB + j * 32, 16, 1024, 2);
+              const uint32_t d = d_tmem + h * C::ACC_COLS;
+              if constexpr (C::SPARSE) {
+                const uint64_t bdesc = smem_desc(b_base + (j >> 1) * C::B_ATOM + (j & 1) * 64, 16, 1024, 2);
+                umma_sparse_cg2<C::KIND>(d, adesc, bdesc, tmem + C::E_COL + 8 * h + 2 * j, C::IDESC, acc_flag);
+              } else {
+                const uint64_t bdesc = smem_desc(b_base + j * 32, 16, 1024, 2);
+                umma_dense_cg2<C::KIND>(d, adesc, bdesc, C::IDESC, acc_flag);
+              }
             }
           }
           tc_commit_mc(&empty[stage], static_cast<uint16_t>((1u << C::CL) - 1));  // every CTA of the cluster
@@ -360,6 +383,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   } else {
     // ------------------------------------------------ epilogue ----
     const uint32_t quarter = warp & 3;  // TMEM lane quarter this warp may access
+    const uint32_t sub = (warp - 2) >> 2;  // M-subtile this warp drains
     const uint32_t lane = lane_id();
     uint8_t* stage_base = smem + C::OFF_EPI + (warp - 2) * C::EPI_WARP;
     int buf = 0;
@@ -368,14 +392,14 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       int ms, nt;
       tile_coords(tile, p, m_super, ms, nt);
       const int mt = ms * C::NPAIR + static_cast<int>(pair);
-      const int acc = it & 1;
-      const uint32_t acc_phase = (it >> 1) & 1;
+      const int acc = C::ACC_STAGES == 2 ? (it & 1) : 0;
+      const uint32_t acc_phase = C::ACC_STAGES == 2 ? ((it >> 1) & 1) : (it & 1);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int64_t row0 = static_cast<int64_t>(mt) * C::BM + rank * C::A_ROWS + quarter * 32;
+      const int64_t row0 = static_cast<int64_t>(mt) * C::BM + sub * 256 + rank * C::A_ROWS + quarter * 32;
       float sc = 0.f;
       if constexpr (C::OUT != SLSP_OUT_RAW_NM) sc = (row0 + lane < p.n) ? __ldg(p.s_ch + row0 + lane) : 0.f;
-      const uint32_t t_base = tmem + ((quarter * 32) << 16) + acc * C::ACC_COLS;
+      const uint32_t t_base = tmem + ((quarter * 32) << 16) + (acc * C::MSUB + sub) * C::ACC_COLS;
 #pragma unroll 1
       for (int c = 0; c < C::BN / 32; ++c) {
         const int64_t t0 = static_cast<int64_t>(nt) * C::BN + c * 32;
@@ -512,7 +536,7 @@ int run(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const 
   attr[0].val.clusterDim.x = C::CL;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
-  cfg.blockDim = dim3(kNumThreads);
+  cfg.blockDim = dim3(C::THREADS);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = s;
   cfg.attrs = attr;
@@ -537,33 +561,43 @@ int run(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const 
   return SLSP_OK;
 }
 
-template <bool SPARSE, MmaKind K, int BN, int ST, int CL>
+// Pipeline depth that fits 227 KB of smem for each configuration.
+constexpr int stages_for(bool sparse, int msub, bool raw) {
+  if (msub == 1) return sparse ? 4 : 6;
+  return sparse ? (raw ? 2 : 3) : (raw ? 3 : 4);
+}
+
+template <bool SPARSE, MmaKind K, int BN, int CL, int MSUB>
 int run_out_cl(int out_mode, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const CUtensorMap& o,
                const Params& p, cudaStream_t s) {
+  constexpr int SR = stages_for(SPARSE, MSUB, true), SB = stages_for(SPARSE, MSUB, false);
   switch (out_mode) {
-    case SLSP_OUT_RAW_NM: return run<Cfg<SPARSE, K, BN, ST, SLSP_OUT_RAW_NM, CL>>(a, b, e, o, p, s);
-    case SLSP_OUT_BF16_NM: return run<Cfg<SPARSE, K, BN, ST, SLSP_OUT_BF16_NM, CL>>(a, b, e, o, p, s);
-    case SLSP_OUT_BF16_MN: return run<Cfg<SPARSE, K, BN, ST, SLSP_OUT_BF16_MN, CL>>(a, b, e, o, p, s);
+    case SLSP_OUT_RAW_NM: return run<Cfg<SPARSE, K, BN, SR, SLSP_OUT_RAW_NM, CL, MSUB>>(a, b, e, o, p, s);
+    case SLSP_OUT_BF16_NM: return run<Cfg<SPARSE, K, BN, SB, SLSP_OUT_BF16_NM, CL, MSUB>>(a, b, e, o, p, s);
+    case SLSP_OUT_BF16_MN: return run<Cfg<SPARSE, K, BN, SB, SLSP_OUT_BF16_MN, CL, MSUB>>(a, b, e, o, p, s);
   }
   return SLSP_ERR_INVALID;
 }
 
-// Cluster shape: 2 (one CTA pair) or 4 (two pairs sharing activation tiles by
-// TMA multicast); env SLSP_GEMM_CLUSTER overrides the per-kernel default.
-template <bool SPARSE, MmaKind K, int BN, int ST>
+// Tile shape knobs: cluster 2 (one CTA pair) or 4 (two pairs sharing
+// activation tiles by TMA multicast), and 1 or 2 M-subtiles per pair; env
+// SLSP_GEMM_CLUSTER / SLSP_GEMM_MSUB override the per-kernel defaults.
+template <bool SPARSE, MmaKind K, int BN>
 int run_out(int out_mode, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const CUtensorMap& o,
-            const Params& p, cudaStream_t s, uint32_t default_cluster) {
-  if (env_knob("SLSP_GEMM_CLUSTER", default_cluster) == 4)
-    return run_out_cl<SPARSE, K, BN, ST, 4>(out_mode, a, b, e, o, p, s);
-  return run_out_cl<SPARSE, K, BN, ST, 2>(out_mode, a, b, e, o, p, s);
+            const Params& p, cudaStream_t s, uint32_t cluster, uint32_t msub) {
+  if (cluster == 4)
+    return msub == 2 ? run_out_cl<SPARSE, K, BN, 4, 2>(out_mode, a, b, e, o, p, s)
+                     : run_out_cl<SPARSE, K, BN, 4, 1>(out_mode, a, b, e, o, p, s);
+  return msub == 2 ? run_out_cl<SPARSE, K, BN, 2, 2>(out_mode, a, b, e, o, p, s)
+                   : run_out_cl<SPARSE, K, BN, 2, 1>(out_mode, a, b, e, o, p, s);
 }
 
 constexpr int kSparseBN = 224;
-constexpr int kSparseStages = 4;
 constexpr int kDenseBN = 256;
-constexpr int kDenseStages = 6;
 constexpr uint32_t kSparseCluster = 2;
 constexpr uint32_t kDenseCluster = 2;
+constexpr uint32_t kSparseMsub = 1;
+constexpr uint32_t kDenseMsub = 1;
 
 int check_out(int out_mode, const float* s_ch, const float* s_tok, void* out, int64_t ldo, int64_t n, int64_t m) {
   if (!out) return SLSP_ERR_INVALID;
@@ -599,7 +633,11 @@ int slsp_sparse_gemm(int dtype, const void* values, const uint8_t* meta, int64_t
   CUtensorMap ta, tb, te, to;
   Params p{};
   if ((st = make_map_2d(&ta, values, kp / 2, n, 128))) return st;
-  if ((st = make_map_2d(&tb, act, kp, m, kSparseBN / 2))) return st;
+  // activation box: the CTA's half of the N tile, split once more across the
+  // pairs of a 4-CTA cluster (each pair fetches one slice and multicasts it)
+  const uint32_t cluster = env_knob("SLSP_GEMM_CLUSTER", kSparseCluster);
+  const uint32_t msub = env_knob("SLSP_GEMM_MSUB", kSparseMsub);
+  if ((st = make_map_2d(&tb, act, kp, m, kSparseBN / 2 / (cluster / 2)))) return st;
   if ((st = make_map_meta(&te, meta, n, kp))) return st;
   if ((st = make_map_out(&to, out, out_mode, n, m, ldo, &p.tma_store))) return st;
   p.n = n;
@@ -613,8 +651,8 @@ int slsp_sparse_gemm(int dtype, const void* values, const uint8_t* meta, int64_t
   p.hints = env_knob("SLSP_GEMM_HINTS", kDefaultHints);
   p.group = static_cast<int>(env_knob("SLSP_GEMM_GROUP", 8));
   if (dtype == SLSP_DT_I8)
-    return run_out<true, MmaKind::I8, kSparseBN, kSparseStages>(out_mode, ta, tb, te, to, p, s, kSparseCluster);
-  return run_out<true, MmaKind::F8, kSparseBN, kSparseStages>(out_mode, ta, tb, te, to, p, s, kSparseCluster);
+    return run_out<true, MmaKind::I8, kSparseBN>(out_mode, ta, tb, te, to, p, s, cluster, msub);
+  return run_out<true, MmaKind::F8, kSparseBN>(out_mode, ta, tb, te, to, p, s, cluster, msub);
 }
 
 int slsp_dense_gemm(int dtype, const void* w, int64_t n, int64_t k, const void* act, int64_t m, const float* s_ch,
@@ -634,7 +672,9 @@ int slsp_dense_gemm(int dtype, const void* w, int64_t n, int64_t k, const void* 
   CUtensorMap ta, tb, to;
   Params p{};
   if ((st = make_map_2d(&ta, w, k * esz, n, 128))) return st;
-  if ((st = make_map_2d(&tb, act, k * esz, m, kDenseBN / 2))) return st;
+  const uint32_t cluster = env_knob("SLSP_GEMM_CLUSTER", kDenseCluster);
+  const uint32_t msub = env_knob("SLSP_GEMM_MSUB", kDenseMsub);
+  if ((st = make_map_2d(&tb, act, k * esz, m, kDenseBN / 2 / (cluster / 2)))) return st;
   if ((st = make_map_out(&to, out, out_mode, n, m, ldo, &p.tma_store))) return st;
   p.n = n;
   p.m = m;
@@ -647,10 +687,10 @@ int slsp_dense_gemm(int dtype, const void* w, int64_t n, int64_t k, const void* 
   p.hints = env_knob("SLSP_GEMM_HINTS", kDefaultHints);
   p.group = static_cast<int>(env_knob("SLSP_GEMM_GROUP", 8));
   if (dtype == SLSP_DT_I8)
-    return run_out<false, MmaKind::I8, kDenseBN, kDenseStages>(out_mode, ta, tb, ta, to, p, s, kDenseCluster);
+    return run_out<false, MmaKind::I8, kDenseBN>(out_mode, ta, tb, ta, to, p, s, cluster, msub);
   if (dtype == SLSP_DT_E4M3)
-    return run_out<false, MmaKind::F8, kDenseBN, kDenseStages>(out_mode, ta, tb, ta, to, p, s, kDenseCluster);
-  return run_out<false, MmaKind::F16, kDenseBN, kDenseStages>(out_mode, ta, tb, ta, to, p, s, kDenseCluster);
+    return run_out<false, MmaKind::F8, kDenseBN>(out_mode, ta, tb, ta, to, p, s, cluster, msub);
+  return run_out<false, MmaKind::F16, kDenseBN>(out_mode, ta, tb, ta, to, p, s, cluster, msub);
 }
 
 }  // extern "C"

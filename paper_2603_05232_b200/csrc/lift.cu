@@ -202,6 +202,26 @@ SLSP_DEVINL float elem(const uint4 (&v)[N], int e) {
   return __uint_as_float(((w[e >> 1] >> (16 * (e & 1))) & 0xFFFFu) << 16);
 }
 
+// Exact f32 -> f64 widening on the integer pipes (the FP64 pipe is the
+// lifting kernel's bottleneck). Zero/subnormal/non-finite inputs take the
+// conversion instruction.
+SLSP_DEVINL double widen_exact(float f) {
+  const uint32_t u = __float_as_uint(f);
+  const uint32_t e = (u >> 23) & 0xFFu;
+  if (e == 0u || e == 0xFFu) return static_cast<double>(f);
+  const uint32_t hi = (u & 0x80000000u) | ((e + 896u) << 20) | ((u >> 3) & 0xFFFFFu);
+  return __hiloint2double(static_cast<int>(hi), static_cast<int>(u << 29));
+}
+
+// quantize.hpp:30-37 for one element. INT8: |x| <= absmax implies
+// |x*r| <= fl(absmax*fl(127/absmax)) < 127.5, so the reference's clamp never
+// binds and rint+convert is one cvt.rni (ties-to-even, like nearbyint).
+template <int KIND>
+SLSP_DEVINL uint32_t quant_code(float x, double r) {
+  if constexpr (KIND == K_INT8) return static_cast<uint32_t>(__double2int_rn(widen_exact(x) * r)) & 0xFFu;
+  return quantize_value(static_cast<double>(x) * r, KIND);
+}
+
 template <int IN, int KIND, int L>
 __global__ void __launch_bounds__(256) act_warp_kernel(ActArgs a) {
   using G = WarpGeom<IN, KIND, L>;
@@ -252,9 +272,7 @@ __global__ void __launch_bounds__(256) act_warp_kernel(ActArgs a) {
 #pragma unroll
         for (int i = 0; i < G::ELEMS / 4 + 1; ++i) qw[i] = 0;
 #pragma unroll
-        for (int e = 0; e < G::ELEMS; ++e)
-          qw[e >> 2] |= static_cast<uint32_t>(quantize_value(static_cast<double>(elem<IN>(v, e)) * r, KIND))
-                        << (8 * (e & 3));
+        for (int e = 0; e < G::ELEMS; ++e) qw[e >> 2] |= quant_code<KIND>(elem<IN>(v, e), r) << (8 * (e & 3));
 #pragma unroll
         for (int g = 0; g < 4; ++g)
 #pragma unroll

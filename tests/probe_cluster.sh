@@ -1,10 +1,10 @@
 #!/bin/bash
 # Cluster-of-4 (multicast B) vs cluster-of-2, both kernels; correctness first.
 out=${1:-gpurun_out}
-for cl in 2 4; do
-  SLSP_GEMM_CLUSTER=$cl timeout 300 python -m pytest tests/test_gpu_gemm.py -q -x 2>&1 | tail -2
-  for grp in 8 16 32; do
-    SLSP_GEMM_CLUSTER=$cl SLSP_GEMM_GROUP=$grp timeout 300 python bench.py --steps 3 --warmup 1 --no-e2e --no-cpu > $out/cl_${cl}_$grp.json 2>$out/cl_${cl}_$grp.err
+for cl in ${CLS:-4 2}; do
+  SLSP_GEMM_CLUSTER=$cl timeout 120 python -m pytest tests/test_gpu_gemm.py -q -x 2>&1 | tail -2
+  for grp in ${GRPS:-16 32}; do
+    SLSP_GEMM_CLUSTER=$cl SLSP_GEMM_GROUP=$grp timeout 120 python bench.py --steps 3 --warmup 1 --no-e2e --no-cpu > $out/cl_${cl}_$grp.json 2>$out/cl_${cl}_$grp.err
     python - "$out/cl_${cl}_$grp.json" "$cl" "$grp" <<'PY'
 import json, sys
 d = json.load(open(sys.argv[1]))

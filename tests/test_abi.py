@@ -92,3 +92,11 @@ def test_no_device_fails_loudly(native):
     if torch.cuda.is_available():
         pytest.skip("has a GPU")
     assert native.slsp_device_supported(0) == 0
+
+
+def test_cpp_dropin_headers_compile():
+    """include/slsp/*.hpp (the C++ drop-in) compile against the C ABI header."""
+    import subprocess
+
+    r = subprocess.run(["make", "-s", "-C", str(ROOT / "tests" / "cpp")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
