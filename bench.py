@@ -258,6 +258,7 @@ def run_b200(args, world, rank, local):
 
     sp_lift, sp_gemm = per_op(sparse_op_graphs)
     de_lift, de_gemm = per_op(dense_op_graphs) if dense_op_graphs else (None, None)
+    pack = None if args.no_dense else time_pack(slsp, torch, layers, z, l, timed, per_op, stream)
 
     def reduce_max(v):
         if world == 1 or v is None:
@@ -349,7 +350,7 @@ def run_b200(args, world, rank, local):
         "dense": {"value": round(dense_value, 2) if dense_value else None,
                   "ms_per_step": round(de_ms_max, 4) if de_ms_max else None,
                   "kernel": "gemm_kernel<dense,i8> (tcgen05.mma kind::i8 cta_group::2), our own"},
-        "roofline": roofline, "lift_roofline": lift_roofline, "layers": layer_rows,
+        "roofline": roofline, "lift_roofline": lift_roofline, "pack_roofline": pack, "layers": layer_rows,
         "e2e": e2e, "clocks": clocks.result(),
         "gpu_launches": 2 * len(layers) * args.steps,
     }
@@ -361,6 +362,38 @@ def run_b200(args, world, rank, local):
         print(json.dumps(result), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def time_pack(slsp, torch, layers, z, l, timed, per_op, stream):
+    """Offline packer Φ (slsp_pack_compress into preallocated MMA-format
+    buffers, no status check) on the largest layer; HBM roofline."""
+    import ctypes as C
+
+    from paper_2603_05232_b200 import _native as N
+
+    L = max(layers, key=lambda x: x.n * x.k)
+    vals = torch.empty_like(L.packed.values)
+    meta = torch.empty_like(L.packed.meta)
+    lib = N.lib()
+
+    def op():
+        lib.slsp_pack_compress(N.DT_I8, C.c_void_p(L.w.data_ptr()), L.n, L.k, z, l, L.kp,
+                               C.c_void_p(vals.data_ptr()), C.c_void_p(meta.data_ptr()), None, None, None,
+                               C.c_void_p(torch.cuda.current_stream().cuda_stream))
+
+    op()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        op()
+    (ms,), _ = per_op([g, g])  # two identical graphs -> first/second slots
+    ok = torch.equal(vals, L.packed.values) and torch.equal(meta, L.packed.meta)
+    bytes_ = L.n * L.k + L.n * L.kp // 2 + L.n * L.kp // 8
+    peaks = json.loads(PEAKS_FILE.read_text()) if PEAKS_FILE.exists() else {}
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    return {"layer": L.name, "n": L.n, "k": L.k, "ms": round(ms, 4), "bytes": bytes_,
+            "achieved_gbs": round(bytes_ / (ms * 1e-3) / 1e9, 1), "peak_gbs": hbm,
+            "frac": round(bytes_ / (ms * 1e-3) / 1e9 / hbm, 4), "matches_packed": bool(ok)}
 
 
 def run_e2e(slsp, torch, layers, xs, outs, out_mode, z, l, stream, device, args, world, total_flops, reduce_max):

@@ -82,10 +82,13 @@ struct Cfg {
   static_assert(!SPARSE || E_COL + 8 * MSUB <= TMEM_COLS, "TMEM budget: accumulators + metadata");
   static_assert(SPARSE || E_COL <= TMEM_COLS, "TMEM budget: accumulators");
   static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "cta_group::2 N");
-  // epilogue staging: per warp, EPI_BUFS tiles of 32 rows x 32 columns
+  // epilogue: chunks of 32 rows x EPI_COLS columns, double-buffered smem
+  // staging per warp (a TMA store reads one buffer while the next is filled)
   static constexpr int OUT_ESZ = OUT == SLSP_OUT_RAW_NM ? 4 : 2;
-  static constexpr int EPI_BUFS = (OUT == SLSP_OUT_RAW_NM || MSUB == 2) ? 1 : 2;
-  static constexpr int EPI_BUF = 32 * 32 * OUT_ESZ;
+  static constexpr int EPI_COLS = MSUB == 2 ? 16 : 32;
+  static constexpr int EPI_BUFS = 2;
+  static constexpr int EPI_BUF = 32 * EPI_COLS * OUT_ESZ;
+  static constexpr int EPI_ROW = EPI_COLS * OUT_ESZ;  // staging row bytes (NM layout) = swizzle span
   static constexpr int EPI_WARP = EPI_BUFS * EPI_BUF;
   static constexpr int OFF_A = 0;
   static constexpr int OFF_B = OFF_A + STAGES * A_STAGE;
@@ -110,6 +113,7 @@ struct Params {
   void* out;
   int64_t ldo;
   int tma_store;      // 1: swizzled smem staging + TMA store; 0: direct stores
+  int direct_vec;     // with tma_store == 0: rows are 16-byte aligned, use vector stores
   uint32_t debug;
   uint32_t hints;     // kHint* L2 policies
   int group;          // weight tiles per raster band
@@ -143,22 +147,28 @@ SLSP_DEVINL uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-// One 32-row x 32-column chunk of the accumulator (lane = row) to its output.
+// One 32-row x EPI_COLS-column chunk of the accumulator (lane = row) to its
+// output. TMA path: the chunk is staged in smem in the output's 128B/64B/32B
+// swizzle (chunk index ^= row bits, conflict-free 16-byte stores) and written
+// with one bulk tensor store.
 template <typename C>
-SLSP_DEVINL void epilogue_chunk(const Params& p, const CUtensorMap* tmOut, uint8_t* stage, uint32_t (&r)[32],
-                                int64_t row0, int64_t t0, float sc) {
+SLSP_DEVINL void epilogue_chunk(const Params& p, const CUtensorMap* tmOut, uint8_t* stage,
+                                uint32_t (&r)[C::EPI_COLS], int64_t row0, int64_t t0, float sc) {
+  constexpr int NC = C::EPI_COLS;
+  constexpr int NW = C::OUT == SLSP_OUT_RAW_NM ? NC : NC / 2;  // 32-bit output words per lane
   const uint32_t lane = lane_id();
   const int64_t row = row0 + lane;
   // per-token scales: one coalesced load, shuffled to every lane
   float st_lane = 0.f;
-  if constexpr (C::OUT != SLSP_OUT_RAW_NM) st_lane = (t0 + lane < p.m) ? __ldg(p.s_tok + t0 + lane) : 0.f;
-  uint32_t w[C::OUT == SLSP_OUT_RAW_NM ? 32 : 16];  // packed output words of this lane's row
+  if constexpr (C::OUT != SLSP_OUT_RAW_NM)
+    st_lane = (lane < NC && t0 + lane < p.m) ? __ldg(p.s_tok + t0 + lane) : 0.f;
+  uint32_t w[NW];
   if constexpr (C::OUT == SLSP_OUT_RAW_NM) {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) w[i] = r[i];
+    for (int i = 0; i < NC; ++i) w[i] = r[i];
   } else {
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
+    for (int i = 0; i < NW; ++i) {
       const float lo = dequant<typename C::Acc>(r[2 * i], sc, __shfl_sync(0xffffffffu, st_lane, 2 * i));
       const float hi = dequant<typename C::Acc>(r[2 * i + 1], sc, __shfl_sync(0xffffffffu, st_lane, 2 * i + 1));
       w[i] = pack_bf16(lo, hi);
@@ -169,25 +179,20 @@ SLSP_DEVINL void epilogue_chunk(const Params& p, const CUtensorMap* tmOut, uint8
   if (p.tma_store) {
     const uint32_t sb = smem_u32(stage);
     if constexpr (C::OUT == SLSP_OUT_BF16_MN) {
-      // token-major tile [32 tokens][32 features] bf16, 64B rows, 64B swizzle
+      // token-major tile [NC tokens][32 features] bf16: 64B rows, 64B swizzle
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
+      for (int i = 0; i < NC; ++i) {
         const uint32_t chunk = (lane >> 3) ^ ((i >> 1) & 3);
-        const uint16_t v = static_cast<uint16_t>(w[i >> 1] >> (16 * (i & 1)));
-        st_shared_u16(sb + i * 64 + chunk * 16 + (lane & 7) * 2, v);
+        st_shared_u16(sb + i * 64 + chunk * 16 + (lane & 7) * 2, static_cast<uint16_t>(w[i >> 1] >> (16 * (i & 1))));
       }
-    } else if constexpr (C::OUT_ESZ == 2) {
-      // [32 rows][32 tokens] bf16: 64B rows, 64B swizzle (chunk ^= (row>>1)&3)
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        st_shared_v4(sb + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4), w[4 * j], w[4 * j + 1], w[4 * j + 2],
-                     w[4 * j + 3]);
     } else {
-      // [32 rows][32 tokens] 32-bit: 128B rows, 128B swizzle (chunk ^= row&7)
+      // [32 rows][NC columns]: EPI_ROW-byte rows, EPI_ROW-byte swizzle
+      constexpr int CH = C::EPI_ROW / 16;                      // 16-byte chunks per row
+      constexpr int SH = C::EPI_ROW == 128 ? 0 : (C::EPI_ROW == 64 ? 1 : 2);
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
-        st_shared_v4(sb + lane * 128 + ((j ^ (lane & 7)) << 4), w[4 * j], w[4 * j + 1], w[4 * j + 2],
-                     w[4 * j + 3]);
+      for (int j = 0; j < CH; ++j)
+        st_shared_v4(sb + lane * C::EPI_ROW + ((j ^ ((lane >> SH) & (CH - 1))) << 4), w[4 * j], w[4 * j + 1],
+                     w[4 * j + 2], w[4 * j + 3]);
     }
     fence_async_smem();
     __syncwarp();
@@ -201,23 +206,33 @@ SLSP_DEVINL void epilogue_chunk(const Params& p, const CUtensorMap* tmOut, uint8
     }
     return;
   }
-  // direct stores (unaligned output strides): predicated, register-resident
   if (row >= p.n) return;
-  const int64_t valid = imin64(32, p.m - t0);
+  const int64_t valid = imin64(NC, p.m - t0);
+  if constexpr (C::OUT != SLSP_OUT_BF16_MN) {
+    // direct 16-byte vector stores of this lane's row segment (NM layouts,
+    // 16-byte aligned rows): no staging, no store-completion waits
+    if (p.direct_vec && valid == NC) {
+      uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(p.out) + (row * p.ldo + t0) * C::OUT_ESZ);
+#pragma unroll
+      for (int j = 0; j < NW / 4; ++j) dst[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+      return;
+    }
+  }
+  // direct stores (unaligned output strides / tails): predicated, register-resident
   if constexpr (C::OUT == SLSP_OUT_RAW_NM) {
     uint32_t* dst = reinterpret_cast<uint32_t*>(p.out) + row * p.ldo + t0;
 #pragma unroll
-    for (int i = 0; i < 32; ++i)
+    for (int i = 0; i < NC; ++i)
       if (i < valid) dst[i] = w[i];
   } else if constexpr (C::OUT == SLSP_OUT_BF16_NM) {
     uint16_t* dst = reinterpret_cast<uint16_t*>(p.out) + row * p.ldo + t0;
 #pragma unroll
-    for (int i = 0; i < 32; ++i)
+    for (int i = 0; i < NC; ++i)
       if (i < valid) dst[i] = static_cast<uint16_t>(w[i >> 1] >> (16 * (i & 1)));
   } else {
     uint16_t* dst = reinterpret_cast<uint16_t*>(p.out) + t0 * p.ldo + row;
 #pragma unroll
-    for (int i = 0; i < 32; ++i)
+    for (int i = 0; i < NC; ++i)
       if (i < valid) dst[i * p.ldo] = static_cast<uint16_t>(w[i >> 1] >> (16 * (i & 1)));
   }
 }
@@ -338,6 +353,9 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
         const int acc = C::ACC_STAGES == 2 ? (it & 1) : 0;
         const uint32_t acc_phase = C::ACC_STAGES == 2 ? ((it >> 1) & 1) : (it & 1);
+        // MSUB=1: double-buffered accumulators, tempty[acc]. MSUB=2: one
+        // buffer per subtile and a barrier per subtile, so subtile 0 of this
+        // tile starts while the epilogue is still draining subtile 1 of the last.
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem + acc * C::MSUB * C::ACC_COLS;
@@ -356,10 +374,14 @@ __global__ void __launch_bounds__(C::THREADS, 1)
                                      smem_desc(e_base + h * C::E_SUB + c * 2048, 2048, 128, 0));
           }
 #pragma unroll
-          for (int j = 0; j < C::MMAS; ++j) {
-            const uint32_t acc_flag = (kb | j) != 0;
+          for (int h = 0; h < C::MSUB; ++h) {
+            if (C::MSUB == 2 && h == 1 && kb == 0) {  // subtile 1's accumulator must be drained too
+              mbar_wait(&tempty[1], acc_phase ^ 1);
+              tc_fence_after();
+            }
 #pragma unroll
-            for (int h = 0; h < C::MSUB; ++h) {
+            for (int j = 0; j < C::MMAS; ++j) {
+              const uint32_t acc_flag = (kb | j) != 0;
               const uint64_t adesc = smem_desc(a_base + h * C::A_SUB + j * 32, 16, 1024, 2);
               const uint32_t d = d_tmem + h * C::ACC_COLS;
               if constexpr (C::SPARSE) {
@@ -383,7 +405,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   } else {
     // ------------------------------------------------ epilogue ----
     const uint32_t quarter = warp & 3;  // TMEM lane quarter this warp may access
-    const uint32_t sub = (warp - 2) >> 2;  // M-subtile this warp drains
+    const uint32_t sub = (warp - 2) >> 2;  // MSUB=2: which alternate chunks of a subtile this warp drains
     const uint32_t lane = lane_id();
     uint8_t* stage_base = smem + C::OFF_EPI + (warp - 2) * C::EPI_WARP;
     int buf = 0;
@@ -396,27 +418,32 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       const uint32_t acc_phase = C::ACC_STAGES == 2 ? ((it >> 1) & 1) : (it & 1);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int64_t row0 = static_cast<int64_t>(mt) * C::BM + sub * 256 + rank * C::A_ROWS + quarter * 32;
-      float sc = 0.f;
-      if constexpr (C::OUT != SLSP_OUT_RAW_NM) sc = (row0 + lane < p.n) ? __ldg(p.s_ch + row0 + lane) : 0.f;
-      const uint32_t t_base = tmem + ((quarter * 32) << 16) + (acc * C::MSUB + sub) * C::ACC_COLS;
+      // MSUB=2: all 8 warps drain subtile 0 (two warps per lane quarter,
+      // alternating chunks), release it, then subtile 1.
 #pragma unroll 1
-      for (int c = 0; c < C::BN / 32; ++c) {
-        const int64_t t0 = static_cast<int64_t>(nt) * C::BN + c * 32;
-        if (t0 >= p.m) break;  // warp-uniform
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(t_base + c * 32, r);
-        tmem_ld_wait();
-        if (p.tma_store) {
-          if (lane == 0) bulk_wait_read<C::EPI_BUFS - 1>();  // staging buffer free again
-          __syncwarp();
+      for (int h = 0; h < C::MSUB; ++h) {
+        const int64_t row0 = static_cast<int64_t>(mt) * C::BM + h * 256 + rank * C::A_ROWS + quarter * 32;
+        float sc = 0.f;
+        if constexpr (C::OUT != SLSP_OUT_RAW_NM) sc = (row0 + lane < p.n) ? __ldg(p.s_ch + row0 + lane) : 0.f;
+        const uint32_t t_base = tmem + ((quarter * 32) << 16) + (acc * C::MSUB + h) * C::ACC_COLS;
+#pragma unroll 1
+        for (int c = static_cast<int>(sub); c < C::BN / C::EPI_COLS; c += C::MSUB) {
+          const int64_t t0 = static_cast<int64_t>(nt) * C::BN + c * C::EPI_COLS;
+          if (t0 >= p.m) break;  // warp-uniform
+          uint32_t r[C::EPI_COLS];
+          tmem_ld_cols(t_base + c * C::EPI_COLS, r);
+          tmem_ld_wait();
+          if (p.tma_store) {
+            if (lane == 0) bulk_wait_read<C::EPI_BUFS - 1>();  // staging buffer free again
+            __syncwarp();
+          }
+          epilogue_chunk<C>(p, &tmOut, stage_base + buf * C::EPI_BUF, r, row0, t0, sc);
+          if (C::EPI_BUFS == 2) buf ^= 1;
         }
-        epilogue_chunk<C>(p, &tmOut, stage_base + buf * C::EPI_BUF, r, row0, t0, sc);
-        if (C::EPI_BUFS == 2) buf ^= 1;
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[C::MSUB == 2 ? h : acc]), lead));
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), lead));
     }
     if (lane == 0) bulk_wait<0>();
   }
@@ -457,7 +484,7 @@ uint32_t debug_flags() {
 // Tuning knob from the environment (read per call: cheap, and lets probes vary it).
 uint32_t env_knob(const char* name, uint32_t dflt) {
   const char* e = std::getenv(name);
-  return e ? static_cast<uint32_t>(std::strtoul(e, nullptr, 0)) : dflt;
+  return (e && *e) ? static_cast<uint32_t>(std::strtoul(e, nullptr, 0)) : dflt;
 }
 
 // Byte-addressed 2D map (uint8 elements): rows x row_bytes, box rows x 128 B, 128B swizzle.
@@ -494,7 +521,8 @@ int make_map_meta(CUtensorMap* map, const void* base, uint64_t rows, uint64_t kp
 
 // Output map for the TMA-store epilogue: 32x32 element boxes.
 //   NM: (cols = tokens m, rows = n); MN: (cols = n, rows = tokens m).
-int make_map_out(CUtensorMap* map, void* base, int out_mode, int64_t n, int64_t m, int64_t ldo, int* use_tma) {
+int make_map_out(CUtensorMap* map, void* base, int out_mode, int64_t n, int64_t m, int64_t ldo, int cols,
+                 int* use_tma) {
   const int esz = out_mode == SLSP_OUT_RAW_NM ? 4 : 2;
   *use_tma = 0;
   std::memset(map, 0, sizeof(*map));
@@ -504,15 +532,31 @@ int make_map_out(CUtensorMap* map, void* base, int out_mode, int64_t n, int64_t 
   const bool mn = out_mode == SLSP_OUT_BF16_MN;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(mn ? n : m), static_cast<cuuint64_t>(mn ? m : n)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldo * esz)};
-  cuuint32_t box[2] = {32, 32};
+  // NM: box {cols tokens, 32 rows}, swizzle = row bytes; MN: box {32 features, cols tokens}, 64B rows
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(mn ? 32 : cols), static_cast<cuuint32_t>(mn ? cols : 32)};
   cuuint32_t estr[2] = {1, 1};
+  const int row_bytes = mn ? 64 : cols * esz;
+  const CUtensorMapSwizzle sw = row_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                  : CU_TENSOR_MAP_SWIZZLE_32B;
   CUresult r = enc(map, esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, base, dims,
-                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   esz == 4 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
-                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return SLSP_ERR_CUDA;
   *use_tma = 1;
   return SLSP_OK;
+}
+
+// Epilogue store path: TMA staging (1) or direct 16-byte vector stores (2);
+// env SLSP_GEMM_EPI overrides the default (0 = auto: vectors for the
+// 2-subtile tiles' narrow chunks, TMA otherwise). MN output always uses TMA.
+void select_epilogue(Params& p, int out_mode, uint32_t msub) {
+  const uint32_t epi = env_knob("SLSP_GEMM_EPI", 0);
+  const bool aligned = p.tma_store != 0;  // make_map_out enables TMA iff rows are 16-byte aligned
+  if (out_mode != SLSP_OUT_BF16_MN && aligned && (epi == 2 || (epi == 0 && msub == 2))) {
+    p.tma_store = 0;
+    p.direct_vec = 1;
+  }
 }
 
 int num_sms() {
@@ -598,6 +642,7 @@ constexpr uint32_t kSparseCluster = 2;
 constexpr uint32_t kDenseCluster = 2;
 constexpr uint32_t kSparseMsub = 1;
 constexpr uint32_t kDenseMsub = 1;
+constexpr uint32_t kRasterGroup = 16;  // measured best of {4, 8, 16, 32, 148} on Qwen2.5-7B shapes
 
 int check_out(int out_mode, const float* s_ch, const float* s_tok, void* out, int64_t ldo, int64_t n, int64_t m) {
   if (!out) return SLSP_ERR_INVALID;
@@ -635,11 +680,12 @@ int slsp_sparse_gemm(int dtype, const void* values, const uint8_t* meta, int64_t
   if ((st = make_map_2d(&ta, values, kp / 2, n, 128))) return st;
   // activation box: the CTA's half of the N tile, split once more across the
   // pairs of a 4-CTA cluster (each pair fetches one slice and multicasts it)
-  const uint32_t cluster = env_knob("SLSP_GEMM_CLUSTER", kSparseCluster);
-  const uint32_t msub = env_knob("SLSP_GEMM_MSUB", kSparseMsub);
+  const uint32_t cluster = env_knob("SLSP_GEMM_CLUSTER", kSparseCluster) == 4 ? 4 : 2;
+  const uint32_t msub = env_knob("SLSP_GEMM_MSUB", kSparseMsub) == 2 ? 2 : 1;
   if ((st = make_map_2d(&tb, act, kp, m, kSparseBN / 2 / (cluster / 2)))) return st;
   if ((st = make_map_meta(&te, meta, n, kp))) return st;
-  if ((st = make_map_out(&to, out, out_mode, n, m, ldo, &p.tma_store))) return st;
+  if ((st = make_map_out(&to, out, out_mode, n, m, ldo, msub == 2 ? 16 : 32, &p.tma_store))) return st;
+  select_epilogue(p, out_mode, msub);
   p.n = n;
   p.m = m;
   p.num_kb = static_cast<int>(kp / 256);
@@ -649,7 +695,7 @@ int slsp_sparse_gemm(int dtype, const void* values, const uint8_t* meta, int64_t
   p.ldo = ldo;
   p.debug = debug_flags();
   p.hints = env_knob("SLSP_GEMM_HINTS", kDefaultHints);
-  p.group = static_cast<int>(env_knob("SLSP_GEMM_GROUP", 8));
+  p.group = static_cast<int>(env_knob("SLSP_GEMM_GROUP", kRasterGroup));
   if (dtype == SLSP_DT_I8)
     return run_out<true, MmaKind::I8, kSparseBN>(out_mode, ta, tb, te, to, p, s, cluster, msub);
   return run_out<true, MmaKind::F8, kSparseBN>(out_mode, ta, tb, te, to, p, s, cluster, msub);
@@ -672,10 +718,11 @@ int slsp_dense_gemm(int dtype, const void* w, int64_t n, int64_t k, const void* 
   CUtensorMap ta, tb, to;
   Params p{};
   if ((st = make_map_2d(&ta, w, k * esz, n, 128))) return st;
-  const uint32_t cluster = env_knob("SLSP_GEMM_CLUSTER", kDenseCluster);
-  const uint32_t msub = env_knob("SLSP_GEMM_MSUB", kDenseMsub);
+  const uint32_t cluster = env_knob("SLSP_GEMM_CLUSTER", kDenseCluster) == 4 ? 4 : 2;
+  const uint32_t msub = env_knob("SLSP_GEMM_MSUB", kDenseMsub) == 2 ? 2 : 1;
   if ((st = make_map_2d(&tb, act, k * esz, m, kDenseBN / 2 / (cluster / 2)))) return st;
-  if ((st = make_map_out(&to, out, out_mode, n, m, ldo, &p.tma_store))) return st;
+  if ((st = make_map_out(&to, out, out_mode, n, m, ldo, msub == 2 ? 16 : 32, &p.tma_store))) return st;
+  select_epilogue(p, out_mode, msub);
   p.n = n;
   p.m = m;
   p.num_kb = static_cast<int>(k * esz / 128);
@@ -685,7 +732,7 @@ int slsp_dense_gemm(int dtype, const void* w, int64_t n, int64_t k, const void* 
   p.ldo = ldo;
   p.debug = debug_flags();
   p.hints = env_knob("SLSP_GEMM_HINTS", kDefaultHints);
-  p.group = static_cast<int>(env_knob("SLSP_GEMM_GROUP", 8));
+  p.group = static_cast<int>(env_knob("SLSP_GEMM_GROUP", kRasterGroup));
   if (dtype == SLSP_DT_I8)
     return run_out<false, MmaKind::I8, kDenseBN>(out_mode, ta, tb, ta, to, p, s, cluster, msub);
   if (dtype == SLSP_DT_E4M3)
