@@ -30,13 +30,26 @@ FLAGS = [
 ]
 
 
-def _stale() -> bool:
-    if not LIB.exists():
-        return True
-    mtime = LIB.stat().st_mtime
-    deps = [CSRC / s for s in SOURCES] + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h"))
+def _digest() -> str:
+    import hashlib
+
+    h = hashlib.sha256(" ".join(FLAGS).encode())
+    deps = sorted([CSRC / s for s in SOURCES] + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")))
     deps.append(ROOT / "include" / "slsp_b200.h")
-    return any(d.stat().st_mtime > mtime for d in deps)
+    for d in deps:
+        h.update(d.name.encode())
+        h.update(d.read_bytes())
+    return h.hexdigest()
+
+
+STAMP = PKG / "_build" / "stamp"
+
+
+def _stale() -> bool:
+    """Content-hash staleness (mtimes are unreliable across edits/snapshots)."""
+    if not LIB.exists() or not STAMP.exists():
+        return True
+    return STAMP.read_text().strip() != _digest()
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
@@ -67,6 +80,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if r.returncode:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("link failed")
+    STAMP.write_text(_digest())
     return LIB
 
 

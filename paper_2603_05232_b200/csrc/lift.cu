@@ -222,6 +222,19 @@ SLSP_DEVINL uint32_t quant_code(float x, double r) {
   return quantize_value(static_cast<double>(x) * r, KIND);
 }
 
+// INT8 fast path, exact: y = fl32(x * fl32(r)) differs from the reference's
+// fl64(x * r) by < 1.6e-5 (|y| <= 127.0001, two fp32 roundings); rounding y
+// with the 1.5*2^23 magic constant therefore gives rint(fl64(x*r)) unless y is
+// within 3e-5 of a half-integer, in which case the FP64 path decides. The
+// code byte is the low byte of the magic sum (0x4B400000 + q).
+SLSP_DEVINL uint32_t quant_int8_fast(float x, float r32, double r) {
+  const float y = __fmul_rn(x, r32);
+  const float t = __fadd_rn(y, 12582912.0f);
+  const float frac = __fsub_rn(y, __fsub_rn(t, 12582912.0f));
+  if (fabsf(frac) >= 0.49997f) return quant_code<K_INT8>(x, r);
+  return __float_as_uint(t) & 0xFFu;
+}
+
 template <int IN, int KIND, int L>
 __global__ void __launch_bounds__(256) act_warp_kernel(ActArgs a) {
   using G = WarpGeom<IN, KIND, L>;
@@ -234,19 +247,38 @@ __global__ void __launch_bounds__(256) act_warp_kernel(ActArgs a) {
     const uint4* src = reinterpret_cast<const uint4*>(a.x + row * a.cols * G::ESZ);
     uint4* dst = reinterpret_cast<uint4*>(a.out + row * a.out_bytes);
     double r = 0.0;
+    float r32 = 0.f;
     if constexpr (KIND != K_NONE) {
       float amax = 0.f;
       int bad = 0;
+      if constexpr (IN == IN_BF16) {
+        // packed bf16x2 |x| max; NaN propagates and Inf wins, so the row is
+        // non-finite iff the final max is
+        __nv_bfloat162 m2 = __float2bfloat162_rn(0.f);
 #pragma unroll 2
-      for (int q = lane; q < nquads; q += 32) {
-        uint4 v[G::IN_VEC];
+        for (int q = lane; q < nquads; q += 32) {
+          uint4 v[G::IN_VEC];
 #pragma unroll
-        for (int i = 0; i < G::IN_VEC; ++i) v[i] = __ldg(src + q * G::IN_VEC + i);
+          for (int i = 0; i < G::IN_VEC; ++i) v[i] = __ldg(src + q * G::IN_VEC + i);
+          const uint32_t* w = reinterpret_cast<const uint32_t*>(v);
 #pragma unroll
-        for (int e = 0; e < G::ELEMS; ++e) {
-          const float f = elem<IN>(v, e);
-          bad |= !isfinite(f);
-          amax = fmaxf(amax, fabsf(f));
+          for (int e = 0; e < G::IN_VEC * 4; ++e)
+            m2 = __hmax2_nan(m2, __habs2(*reinterpret_cast<const __nv_bfloat162*>(&w[e])));
+        }
+        amax = fmaxf(__low2float(m2), __high2float(m2));
+        bad = !isfinite(__low2float(m2)) || !isfinite(__high2float(m2));
+      } else {
+#pragma unroll 2
+        for (int q = lane; q < nquads; q += 32) {
+          uint4 v[G::IN_VEC];
+#pragma unroll
+          for (int i = 0; i < G::IN_VEC; ++i) v[i] = __ldg(src + q * G::IN_VEC + i);
+#pragma unroll
+          for (int e = 0; e < G::ELEMS; ++e) {
+            const float f = elem<IN>(v, e);
+            bad |= !isfinite(f);
+            amax = fmaxf(amax, fabsf(f));
+          }
         }
       }
 #pragma unroll
@@ -259,6 +291,7 @@ __global__ void __launch_bounds__(256) act_warp_kernel(ActArgs a) {
       const double qmax = KIND == K_INT8 ? 127.0 : 448.0;
       const double absmax = static_cast<double>(amax);
       r = absmax == 0.0 ? 0.0 : qmax / absmax;
+      r32 = __double2float_rn(r);
       if (lane == 0) a.scales[row] = absmax == 0.0 ? 1.0f : __double2float_rn(absmax / qmax);
     }
 #pragma unroll 2
@@ -269,10 +302,19 @@ __global__ void __launch_bounds__(256) act_warp_kernel(ActArgs a) {
       uint32_t o[G::OUT_VEC * 4];
       if constexpr (KIND != K_NONE) {
         uint32_t qw[G::ELEMS / 4 + 1];
+        qw[G::ELEMS / 4] = 0;
 #pragma unroll
-        for (int i = 0; i < G::ELEMS / 4 + 1; ++i) qw[i] = 0;
+        for (int i = 0; i < G::ELEMS / 4; ++i) {
+          uint32_t b[4];
 #pragma unroll
-        for (int e = 0; e < G::ELEMS; ++e) qw[e >> 2] |= quant_code<KIND>(elem<IN>(v, e), r) << (8 * (e & 3));
+          for (int d = 0; d < 4; ++d) {
+            const float x = elem<IN>(v, 4 * i + d);
+            if constexpr (KIND == K_INT8) b[d] = quant_int8_fast(x, r32, r);
+            else b[d] = quant_code<KIND>(x, r);
+          }
+          // byte 0 of each b[d] -> byte d of the word
+          qw[i] = __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
+        }
 #pragma unroll
         for (int g = 0; g < 4; ++g)
 #pragma unroll

@@ -235,6 +235,118 @@ __global__ void prune_kernel(const uint8_t* w, int64_t rows, int64_t cols, int z
   }
 }
 
+// ---------------------------------------------------------------------------
+// 6:8 fast path. The greedy placement (pack.hpp:94-111) plus compress's
+// canonical padding (gemm.hpp:99-102) is a pure function of the block's 8-bit
+// nonzero mask, so it is tabulated once on the host (build_lut8, the same
+// greedy) into 256 entries: per window w, bits [16w, 16w+12) hold the 2-bit
+// code pair (4 bits) and the source offsets of the two value slots (4 bits
+// each, 8 = padding zero). A thread packs 8 consecutive blocks from 4*ESZ
+// 16-byte loads into 48*ESZ value bytes and 12 metadata bytes (vector stores).
+struct Lut8 {
+  unsigned long long e[256];
+};
+
+Lut8 build_lut8() {
+  Lut8 t{};
+  for (int mask = 0; mask < 256; ++mask) {
+    unsigned used = 0;
+    unsigned long long entry = 0;
+    for (int w = 0; w < 3; ++w) {
+      int p[2] = {-1, -1}, cnt = 0;
+      for (int d = 0; d < 4; ++d) {
+        const int k = 2 * w + d;
+        if (((mask >> k) & 1) && !((used >> k) & 1) && cnt < 2) {
+          used |= 1u << k;
+          p[cnt++] = d;
+        }
+      }
+      int c0, c1, s0 = 8, s1 = 8;  // codes and value sources (8 = zero)
+      if (cnt == 2) {
+        c0 = p[0], c1 = p[1], s0 = 2 * w + p[0], s1 = 2 * w + p[1];
+      } else if (cnt == 1) {
+        if (p[0] == 0) c0 = 0, c1 = 1, s0 = 2 * w;
+        else c0 = 0, c1 = p[0], s1 = 2 * w + p[0];
+      } else {
+        c0 = 0, c1 = 1;
+      }
+      const unsigned long long f = static_cast<unsigned long long>((c0 | (c1 << 2)) | (s0 << 4) | (s1 << 8));
+      entry |= f << (16 * w);
+    }
+    t.e[mask] = entry;
+  }
+  return t;
+}
+
+template <int ESZ>
+__global__ void __launch_bounds__(256) pack68_kernel(const uint8_t* __restrict__ w, int64_t rows, int64_t cols,
+                                                     int z, int dtype, Lut8 lut, uint8_t* __restrict__ values,
+                                                     int64_t ld_vals, uint8_t* __restrict__ meta, int64_t ld_meta,
+                                                     unsigned long long* status) {
+  __shared__ unsigned long long s_lut[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) s_lut[i] = lut.e[i];
+  __syncthreads();
+  const int64_t octs = cols / 64;  // 8 blocks of 8 per thread
+  const int64_t total = rows * octs;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t row = idx / octs, q = idx - row * octs;
+    const uint4* src = reinterpret_cast<const uint4*>(w + (row * cols + q * 64) * ESZ);
+    uint4 v[4 * ESZ];
+#pragma unroll
+    for (int i = 0; i < 4 * ESZ; ++i) v[i] = __ldg(src + i);
+    const unsigned long long* x = reinterpret_cast<const unsigned long long*>(v);  // 8*ESZ bytes per block
+    uint32_t ov[12 * ESZ];
+    uint32_t om[3] = {0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < 12 * ESZ; ++i) ov[i] = 0;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+      uint32_t mask = 0;
+      if constexpr (ESZ == 1) {
+        // byte b nonzero (e4m3: ignoring the sign bit) -> bit b
+        const unsigned long long m7 = 0x7F7F7F7F7F7F7F7Full;
+        const unsigned long long b = dtype == SLSP_DT_E4M3 ? (x[g] & m7) : x[g];
+        const unsigned long long t = (((b & m7) + m7) | b) & 0x8080808080808080ull;
+        mask = static_cast<uint32_t>(((t >> 7) * 0x0102040810204080ull) >> 56);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const unsigned long long h = x[2 * g + (e >> 2)] >> (16 * (e & 3));
+          mask |= ((h & 0x7FFFull) != 0 ? 1u : 0u) << e;
+        }
+      }
+      if (__popc(mask) > z) record_error(status, row, q * 8 + g);  // first_overfull_block
+      const unsigned long long ent = s_lut[mask];
+#pragma unroll
+      for (int wi = 0; wi < 3; ++wi) {
+        const uint32_t f = static_cast<uint32_t>(ent >> (16 * wi));
+        const int ni = g * 3 + wi;  // nibble index within the thread's 24 windows
+        om[ni >> 3] |= (f & 0xFu) << (4 * (ni & 7));
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          const uint32_t so = (f >> (4 + 4 * s)) & 0xFu;
+          uint32_t val = 0;
+          if constexpr (ESZ == 1) {
+            if (so < 8) val = static_cast<uint32_t>(x[g] >> (8 * so)) & 0xFFu;
+          } else {
+            if (so < 8) val = static_cast<uint32_t>(x[2 * g + (so >> 2)] >> (16 * (so & 3))) & 0xFFFFu;
+          }
+          const int vi = (g * 6 + wi * 2 + s) * ESZ;  // byte index in the thread's value run
+          ov[vi >> 2] |= val << (8 * (vi & 3));
+        }
+      }
+    }
+    uint4* dv = reinterpret_cast<uint4*>(values + row * ld_vals + q * 48 * ESZ);
+#pragma unroll
+    for (int i = 0; i < 3 * ESZ; ++i) dv[i] = make_uint4(ov[4 * i], ov[4 * i + 1], ov[4 * i + 2], ov[4 * i + 3]);
+    uint32_t* dm = reinterpret_cast<uint32_t*>(meta + row * ld_meta + q * 12);
+    dm[0] = om[0];
+    dm[1] = om[1];
+    dm[2] = om[2];
+  }
+}
+
 // Row-major 2-bit codes -> MMA-tiled metadata (see slsp_tile_meta in the
 // header): one 16-byte chunk per thread, coalesced on the tiled side.
 __global__ void tile_meta_kernel(const uint8_t* __restrict__ meta, int64_t rows, int64_t kp, uint8_t* tiled) {
@@ -340,6 +452,31 @@ int slsp_pack_compress(int dtype, const void* w, int64_t rows, int64_t cols, int
   if ((st = require_sm100())) return st;
   if ((st = status_reset(status_ws, s))) return st;
   unsigned long long* status = static_cast<unsigned long long*>(status_ws);  // may be null: no report
+  // 6:8 fast path (table-driven greedy, 8 blocks per thread, vector I/O)
+  const int64_t ld_vals = kp / 2 * esz, ld_meta = kp / 8;
+  if (l == 8 && cols % 64 == 0 && ld_vals % 16 == 0 && ld_meta % 4 == 0 && rows > 0 &&
+      !((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(values) | reinterpret_cast<uintptr_t>(meta)) &
+        15u)) {
+    static const Lut8 lut = build_lut8();
+    const int64_t threads = rows * (cols / 64);
+    if (threads > 0) {
+      const unsigned grid = grid_for(threads, 256);
+      const auto* in = static_cast<const uint8_t*>(w);
+      auto* out = static_cast<uint8_t*>(values);
+      if (esz == 1)
+        pack68_kernel<1><<<grid, 256, 0, s>>>(in, rows, cols, z, dtype, lut, out, ld_vals, meta, ld_meta, status);
+      else
+        pack68_kernel<2><<<grid, 256, 0, s>>>(in, rows, cols, z, dtype, lut, out, ld_vals, meta, ld_meta, status);
+      SLSP_LAUNCH_CHECK();
+    }
+    const int64_t kprime_b = kprime / 2 * esz;  // padding windows past K': zero values, codes (0,1)
+    if (ld_vals > kprime_b) {
+      SLSP_CUDA_TRY(cudaMemset2DAsync(static_cast<uint8_t*>(values) + kprime_b, ld_vals, 0, ld_vals - kprime_b,
+                                      rows, s));
+      SLSP_CUDA_TRY(cudaMemset2DAsync(meta + kprime / 8, ld_meta, 0x44, ld_meta - kprime / 8, rows, s));
+    }
+    return status_collect(status_ws, s, SLSP_ERR_NOT_COMPLIANT, err_row, err_block);
+  }
   PackArgs a{};
   a.w = static_cast<const uint8_t*>(w);
   a.rows = rows;
