@@ -5,6 +5,7 @@
 out=${1:-gpurun_out}
 timeout 900 python -m pytest tests -m gpu -q > $out/pytest_round.log 2>&1; echo "pytest exit $?" >> $out/pytest_round.log
 tail -3 $out/pytest_round.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print(\"smoke ok\")" > $out/smoke.log 2>&1; tail -2 $out/smoke.log
 timeout 600 python bench.py --steps 10 --warmup 3 > $out/bench_round.json 2> $out/bench_round.err; echo "bench exit $?"
 timeout 300 python bench.py --impl reference --steps 3 --warmup 1 > $out/bench_ref.json 2> $out/bench_ref.err; echo "ref exit $?"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches.csv \
@@ -16,6 +17,6 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm
    python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu > $out/ncu_d.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:act_warp_kernel -s 4 -c 1 -o $out/prof_lift \
    python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu --no-dense > $out/ncu_l.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:pack_kernel -s 0 -c 1 -o $out/prof_pack \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:pack68_kernel -s 0 -c 1 -o $out/prof_pack \
    python tests/probe_pack.py > $out/ncu_p.log 2>&1
 echo done
