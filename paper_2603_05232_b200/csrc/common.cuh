@@ -64,10 +64,12 @@ SLSP_DEVINL void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// Arrive on a barrier that may live in another CTA of the cluster.
+// Arrive on a barrier that may live in another CTA of the cluster. Default
+// (.release.cta) semantics: used to hand TMEM back to the MMA warp, which
+// reads no memory the arriving threads wrote (the tcgen05 fences order the
+// TMEM loads); .release.cluster would add MEMBAR.GPU + ERRBAR per arrive.
 SLSP_DEVINL void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
-               : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 
 SLSP_DEVINL void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -320,6 +322,55 @@ SLSP_DEVINL void tmem_ld_cols(uint32_t taddr, uint32_t (&r)[N]) {
 }
 
 SLSP_DEVINL void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// wait::ld that also orders every later use of r after the wait (the
+// registers of an in-flight tcgen05.ld are read-write operands of the wait).
+SLSP_DEVINL void tmem_ld_wait_regs(uint32_t (&r)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                 "+r"(r[15])
+               :
+               : "memory");
+}
+
+SLSP_DEVINL float4 ld_shared_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+
+// Non-blocking probe of an mbarrier phase.
+SLSP_DEVINL bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+// Packed fp32 pair multiply (sm_100 FMUL2): two IEEE round-to-nearest products,
+// bit-identical to two __fmul_rn.
+SLSP_DEVINL float2 fmul2_rn(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 a2, b2, d2;\n\t"
+      "mov.b64 a2, {%2, %3};\n\tmov.b64 b2, {%4, %5};\n\t"
+      "mul.rn.f32x2 d2, a2, b2;\n\tmov.b64 {%0, %1}, d2;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+
+// 32-byte global store (sm_100 STG.256) with an L2 cache-policy hint.
+SLSP_DEVINL void st_global_v8_hint(void* p, const uint32_t (&w)[8], uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8}, %9;" ::"l"(p), "r"(w[0]),
+               "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]), "l"(pol)
+               : "memory");
+}
 
 // ------------------------------------------------------------- numerics --
 // fp8.hpp:25-52 (reference) restated for the device: e4m3fn, RNE in double,

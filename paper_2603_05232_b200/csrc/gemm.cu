@@ -33,18 +33,18 @@ constexpr int kNumThreads = 192;
 
 // Debug knobs (env SLSP_GEMM_DEBUG, read once): bit0 skip output stores,
 // bit1 skip operand loads (MMA on stale smem), bit2 load k-block 0 of tile 0
-// only (L2-resident operands). Results are garbage when set; perf probing only.
-enum : uint32_t { kDbgNoStore = 1u, kDbgNoLoad = 2u, kDbgSameTile = 4u, kDbgNoMeta = 8u };
+// only (L2-resident operands), bit3 skip metadata loads, bit4 skip the MMAs
+// (load pipeline alone). Results are garbage when set; perf probing only.
+enum : uint32_t { kDbgNoStore = 1u, kDbgNoLoad = 2u, kDbgSameTile = 4u, kDbgNoMeta = 8u, kDbgNoMma = 16u };
 // L2 cache-policy hints (env SLSP_GEMM_HINTS overrides kDefaultHints).
 enum : uint32_t { kHintBLast = 1u, kHintAFirst = 2u, kHintOutFirst = 4u };
 constexpr uint32_t kDefaultHints = kHintBLast | kHintOutFirst;
 
-template <bool SPARSE_, MmaKind KIND_, int BN_, int STAGES_, int OUT_, int CL_ = 2, int MSUB_ = 1>
+template <bool SPARSE_, MmaKind KIND_, int BN_, int STAGES_, int OUT_, int CL_ = 2, int MSUB_ = 1, int KH_ = 0>
 struct Cfg {
   static constexpr bool SPARSE = SPARSE_;
   static constexpr MmaKind KIND = KIND_;
   static constexpr int BN = BN_;          // tokens per pair tile (MMA N)
-  static constexpr int STAGES = STAGES_;
   static constexpr int OUT = OUT_;
   // Cluster: CL CTAs = CL/2 CTA pairs on adjacent weight tiles of the same
   // token tile; with 2 pairs each activation (B) box is fetched once from L2
@@ -64,18 +64,26 @@ struct Cfg {
   static constexpr int BM = 256 * MSUB;   // weight rows per pair tile
   static constexpr int A_ROWS = 128;      // per CTA per M-subtile
   static constexpr int B_ROWS = BN / 2;   // tokens per CTA
-  static constexpr int A_SUB = 128 * 128;                    // one 128B-swizzle atom column
+  // Half k-stages (sparse only): 128 lifted bytes per stage instead of 256 —
+  // A rows of 64 B (64B swizzle), one B atom, one metadata atom, 2 MMAs —
+  // so twice as many, half-size stages keep more bytes in flight per SM.
+  static constexpr bool KH = KH_ != 0;
+  static_assert(!KH || SPARSE, "half k-stages are for the sparse kernel");
+  static constexpr int A_ROW = KH ? 64 : 128;                // A bytes per row per stage
+  static constexpr uint32_t A_LAYOUT = KH ? 4u : 2u;         // UMMA desc: SWIZZLE_64B / SWIZZLE_128B
+  static constexpr int A_SUB = 128 * A_ROW;                  // one swizzle-atom column of 128 rows
   static constexpr int A_STAGE = MSUB * A_SUB;
-  static constexpr int B_ATOMS = SPARSE ? 2 : 1;             // B bytes per stage = 2x A bytes for .sp
+  static constexpr int B_ATOMS = SPARSE && !KH ? 2 : 1;      // B bytes per stage = 2x A bytes for .sp
   static constexpr int B_ATOM = B_ROWS * 128;
   static constexpr int B_STAGE = B_ATOM * B_ATOMS;
   static constexpr int B_PART = B_ROWS / NPAIR;  // rows of each B box one pair fetches (multicast)
   static_assert(B_PART % 8 == 0, "multicast slices must be whole 128B-swizzle atoms");
-  static constexpr int E_SUB = SPARSE ? 2 * 128 * 16 : 0;    // two 128x128b metadata atoms
+  static constexpr int E_ATOMS = KH ? 1 : 2;                 // 128x128b metadata atoms per stage and subtile
+  static constexpr int E_SUB = SPARSE ? E_ATOMS * 128 * 16 : 0;
   static constexpr int E_STAGE = MSUB * E_SUB;
   static constexpr int STAGE_TX = A_STAGE + B_STAGE + E_STAGE;
   static constexpr int K_BYTES_B = 128 * B_ATOMS;            // activation bytes consumed per stage
-  static constexpr int MMAS = 4;                             // k-steps per stage
+  static constexpr int MMAS = KH ? 2 : 4;                    // k-steps per stage
   static constexpr int ACC_COLS = BN;                        // 32-bit TMEM columns per accumulator
   static constexpr int E_COL = ACC_STAGES * MSUB * BN;       // metadata columns after the accumulators
   static constexpr int TMEM_COLS = 512;
@@ -89,7 +97,17 @@ struct Cfg {
   static constexpr int EPI_BUFS = 2;
   static constexpr int EPI_BUF = 32 * EPI_COLS * OUT_ESZ;
   static constexpr int EPI_ROW = EPI_COLS * OUT_ESZ;  // staging row bytes (NM layout) = swizzle span
-  static constexpr int EPI_WARP = EPI_BUFS * EPI_BUF;
+  // MSUB=2 with BF16 [N][M] output: register-staged epilogue (each subtile is
+  // dequantised into registers and its TMEM released before any store), no
+  // smem staging.
+  static constexpr bool REG_EPI = MSUB == 2 && OUT == SLSP_OUT_BF16_NM;
+  static constexpr int REG_CHUNKS = BN / 32;  // 16-column chunks per warp per subtile (half the columns)
+  static constexpr int EPI_WARP = REG_EPI ? (BN / 2) * 4 : EPI_BUFS * EPI_BUF;  // REG: s_tok slice
+  // smem ring depth: STAGES_ if given, else as many stages as fit (<= 8)
+  static constexpr int FIXED_SMEM = EPI_WARPS * EPI_WARP + 4 * 8 + 16 + 1024;
+  static constexpr int FIT = (227 * 1024 - FIXED_SMEM) / (STAGE_TX + 16);
+  static constexpr int STAGES = STAGES_ ? STAGES_ : (FIT < 8 ? FIT : 8);
+  static_assert(STAGES >= 2, "pipeline depth");
   static constexpr int OFF_A = 0;
   static constexpr int OFF_B = OFF_A + STAGES * A_STAGE;
   static constexpr int OFF_E = OFF_B + STAGES * B_STAGE;
@@ -113,11 +131,21 @@ struct Params {
   void* out;
   int64_t ldo;
   int tma_store;      // 1: swizzled smem staging + TMA store; 0: direct stores
-  int direct_vec;     // with tma_store == 0: rows are 16-byte aligned, use vector stores
+  int direct_vec;     // direct stores: 0 scalar, 1 rows 16-byte aligned (v4), 2 rows 32-byte aligned (v8)
+  int stok_vec;       // s_tok is 16-byte aligned (float4 loads)
   uint32_t debug;
+  uint32_t store_gap_ns;      // register-staged epilogue: pause between 32-byte store rounds
+  unsigned long long* trace;  // perf probing: per-tile clock64 stamps of CTA 0 (env SLSP_GEMM_TRACE = device ptr)
   uint32_t hints;     // kHint* L2 policies
   int group;          // weight tiles per raster band
 };
+
+// Perf probing: slot `slot` of tile iteration `it` on CTA 0 (16 slots per tile;
+// 8/9 hold the MMA's full-wait and the producer's empty-wait cycles of the tile).
+#define SLSP_TRACE(it, slot)                                                          \
+  do {                                                                                \
+    if (p.trace && blockIdx.x == 0) p.trace[(it) * 16 + (slot)] = clock64();           \
+  } while (0)
 
 // Raster: bands of `group` weight tiles; within a band the weight tile varies
 // fastest, so the clusters running concurrently share activation tiles (B)
@@ -145,6 +173,78 @@ SLSP_DEVINL float dequant(uint32_t raw, float sc, float st) {
 SLSP_DEVINL uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// Compiler barrier on 8 registers: the values are materialised at this point
+// in program order (asm volatile is not reordered against the mbarrier ops).
+SLSP_DEVINL void reg_pin(uint32_t (&w)[8]) {
+  asm volatile("" : "+r"(w[0]), "+r"(w[1]), "+r"(w[2]), "+r"(w[3]), "+r"(w[4]), "+r"(w[5]), "+r"(w[6]), "+r"(w[7]));
+}
+
+// Element-wise BF16 stores of the first `valid` values of a packed row segment.
+__device__ __noinline__ void store_tail_u16(uint16_t* dst, const uint32_t* w, int valid) {
+  for (int i = 0; i < valid; ++i) dst[i] = static_cast<uint16_t>(w[i >> 1] >> (16 * (i & 1)));
+}
+
+// a18 for 16 consecutive tokens whose scales sit in shared memory.
+template <typename Acc>
+SLSP_DEVINL void dequant16_smem(const uint32_t (&r)[16], float sc, uint32_t st_sm, uint32_t (&w)[8]) {
+  float st[16];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float4 v = ld_shared_f4(st_sm + 16 * q);
+    st[4 * q] = v.x;
+    st[4 * q + 1] = v.y;
+    st[4 * q + 2] = v.z;
+    st[4 * q + 3] = v.w;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    float2 a;
+    if constexpr (std::is_same<Acc, int32_t>::value) {
+      a.x = __int2float_rn(static_cast<int32_t>(r[2 * i]));
+      a.y = __int2float_rn(static_cast<int32_t>(r[2 * i + 1]));
+    } else {
+      a.x = __uint_as_float(r[2 * i]);
+      a.y = __uint_as_float(r[2 * i + 1]);
+    }
+    a = fmul2_rn(fmul2_rn(a, make_float2(sc, sc)), make_float2(st[2 * i], st[2 * i + 1]));
+    w[i] = pack_bf16(a.x, a.y);
+  }
+}
+
+// a18 for 16 consecutive tokens of one row, packed FMUL2 (same two rn
+// products per element as dequant()), BF16 pairs out.
+template <typename Acc>
+SLSP_DEVINL void dequant16(const Params& p, const uint32_t (&r)[16], float sc, int64_t t0, uint32_t (&w)[8]) {
+  float st[16];
+  if (p.stok_vec && t0 + 16 <= p.m) {
+    // volatile loads: issued here, in chunk order (not hoisted for all chunks
+    // up front, which would spill)
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];"
+                   : "=f"(st[4 * q]), "=f"(st[4 * q + 1]), "=f"(st[4 * q + 2]), "=f"(st[4 * q + 3])
+                   : "l"(p.s_tok + t0 + 4 * q));
+  } else {  // token tail: int32 bound, one base pointer
+    const int valid = static_cast<int>(imin64(16, p.m - t0));
+    const float* base = p.s_tok + t0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) st[i] = i < valid ? __ldg(base + i) : 0.f;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    float2 a;
+    if constexpr (std::is_same<Acc, int32_t>::value) {
+      a.x = __int2float_rn(static_cast<int32_t>(r[2 * i]));
+      a.y = __int2float_rn(static_cast<int32_t>(r[2 * i + 1]));
+    } else {
+      a.x = __uint_as_float(r[2 * i]);
+      a.y = __uint_as_float(r[2 * i + 1]);
+    }
+    a = fmul2_rn(fmul2_rn(a, make_float2(sc, sc)), make_float2(st[2 * i], st[2 * i + 1]));
+    w[i] = pack_bf16(a.x, a.y);
+  }
 }
 
 // One 32-row x EPI_COLS-column chunk of the accumulator (lane = row) to its
@@ -299,25 +399,34 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       // them (evict_last); weights stream through a raster band.
       const uint64_t pol_b = (p.hints & kHintBLast) ? policy_evict_last() : policy_evict_normal();
       const uint64_t pol_a = (p.hints & kHintAFirst) ? policy_evict_first() : policy_evict_normal();
-      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
+      int it = 0;
+      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
         int ms, nt;
         tile_coords(tile, p, m_super, ms, nt);
         int mt = ms * C::NPAIR + static_cast<int>(pair);
         if (same) mt = nt = 0;
+        long long wait_cycles = 0;
         const int a_row = mt * C::BM + static_cast<int>(rank) * C::A_ROWS;
         const int b_row = nt * C::BN + static_cast<int>(rank) * C::B_ROWS;
         for (int kb = 0; kb < p.num_kb; ++kb) {
           const int kl = same ? 0 : kb;
-          mbar_wait(&empty[stage], phase ^ 1);
+          if (p.trace) {
+            const long long t0 = clock64();
+            mbar_wait(&empty[stage], phase ^ 1);
+            wait_cycles += clock64() - t0;
+          } else {
+            mbar_wait(&empty[stage], phase ^ 1);
+          }
           if (no_load) {
             if (leader) mbar_arrive(&full[stage]);
           } else {
             const bool skip_e = p.debug & kDbgNoMeta;
+            if (p.trace && blockIdx.x == 0 && it < 16 && kb < 256) p.trace[65536 + (it * 256 + kb) * 2] = clock64();
             if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (C::STAGE_TX - (skip_e ? C::E_STAGE : 0)));
             const uint32_t bar = mapa_shared(smem_u32(&full[stage]), lead);
 #pragma unroll
             for (int h = 0; h < C::MSUB; ++h)
-              tma_load_2d_cg2_hint(sA + stage * C::A_STAGE + h * C::A_SUB, &tmA, bar, kl * 128, a_row + h * 256,
+              tma_load_2d_cg2_hint(sA + stage * C::A_STAGE + h * C::A_SUB, &tmA, bar, kl * C::A_ROW, a_row + h * 256,
                                    pol_a);
 #pragma unroll
             for (int at = 0; at < C::B_ATOMS; ++at) {
@@ -335,13 +444,16 @@ __global__ void __launch_bounds__(C::THREADS, 1)
 #pragma unroll
                 for (int h = 0; h < C::MSUB; ++h)
                   tma_load_2d_cg2_hint(sE + stage * C::E_STAGE + h * C::E_SUB, &tmE, bar, 0,
-                                       (((a_row + h * 256) >> 7) * p.num_kb + kl) * 16, pol_a);
+                                       C::KH ? (((a_row + h * 256) >> 7) * (p.num_kb >> 1) + (kl >> 1)) * 16 + (kl & 1) * 8
+                                             : (((a_row + h * 256) >> 7) * p.num_kb + kl) * 16,
+                                       pol_a);
           }
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
+        if (p.trace && blockIdx.x == 0) p.trace[it * 16 + 9] = wait_cycles;
       }
     }
   } else if (warp == 1) {
@@ -350,57 +462,183 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
+      const uint16_t all_ctas = static_cast<uint16_t>((1u << C::CL) - 1);
       for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
         const int acc = C::ACC_STAGES == 2 ? (it & 1) : 0;
         const uint32_t acc_phase = C::ACC_STAGES == 2 ? ((it >> 1) & 1) : (it & 1);
         // MSUB=1: double-buffered accumulators, tempty[acc]. MSUB=2: one
-        // buffer per subtile and a barrier per subtile, so subtile 0 of this
-        // tile starts while the epilogue is still draining subtile 1 of the last.
+        // buffer per subtile and a barrier per subtile; subtile 0 of this tile
+        // starts as soon as the epilogue has released it, and subtile 1's MMAs
+        // for the first (up to STAGES) k-blocks are deferred until its drain
+        // completes, so the drains hide behind the mainloop.
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
+        SLSP_TRACE(it, 0);
         const uint32_t d_tmem = tmem + acc * C::MSUB * C::ACC_COLS;
-        for (int kb = 0; kb < p.num_kb; ++kb) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          const uint32_t a_base = smem_u32(sA + stage * C::A_STAGE);
-          const uint32_t b_base = smem_u32(sB + stage * C::B_STAGE);
+        // subtile h's metadata copy + 4 MMAs for k-block kb held in ring stage st
+        const bool no_mma = p.debug & kDbgNoMma;
+        auto issue = [&](int h, int st, int kb) {
+          if (no_mma) return;
+          const uint32_t a_base = smem_u32(sA + st * C::A_STAGE + h * C::A_SUB);
+          const uint32_t b_base = smem_u32(sB + st * C::B_STAGE);
+          // KH: alternate halves of the subtile's 8 metadata columns between stages
+          const uint32_t e_col = C::E_COL + 8 * h + (C::KH ? 4 * (kb & 1) : 0);
           if constexpr (C::SPARSE) {
-            const uint32_t e_base = smem_u32(sE + stage * C::E_STAGE);
+            const uint32_t e_base = smem_u32(sE + st * C::E_STAGE + h * C::E_SUB);
 #pragma unroll
-            for (int h = 0; h < C::MSUB; ++h)
-#pragma unroll
-              for (int c = 0; c < 2; ++c)
-                tmem_cp_128x128b_cg2(tmem + C::E_COL + 8 * h + 4 * c,
-                                     smem_desc(e_base + h * C::E_SUB + c * 2048, 2048, 128, 0));
+            for (int c = 0; c < C::E_ATOMS; ++c)
+              tmem_cp_128x128b_cg2(tmem + e_col + 4 * c, smem_desc(e_base + c * 2048, 2048, 128, 0));
           }
 #pragma unroll
-          for (int h = 0; h < C::MSUB; ++h) {
-            if (C::MSUB == 2 && h == 1 && kb == 0) {  // subtile 1's accumulator must be drained too
+          for (int j = 0; j < C::MMAS; ++j) {
+            const uint32_t acc_flag = (kb | j) != 0;
+            const uint64_t adesc = smem_desc(a_base + j * 32, 16, 8 * C::A_ROW, C::A_LAYOUT);
+            const uint32_t d = d_tmem + h * C::ACC_COLS;
+            if constexpr (C::SPARSE) {
+              const uint64_t bdesc = smem_desc(b_base + (j >> 1) * C::B_ATOM + (j & 1) * 64, 16, 1024, 2);
+              umma_sparse_cg2<C::KIND>(d, adesc, bdesc, tmem + e_col + 2 * j, C::IDESC, acc_flag);
+            } else {
+              const uint64_t bdesc = smem_desc(b_base + j * 32, 16, 1024, 2);
+              umma_dense_cg2<C::KIND>(d, adesc, bdesc, C::IDESC, acc_flag);
+            }
+          }
+        };
+        bool sub1_ready = C::MSUB == 1;
+        long long wait_cycles = 0;
+        int lag = 0, lag_stage = 0, lag_kb = 0;  // deferred subtile-1 k-blocks (consecutive ring stages)
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          if (p.trace) {
+            const long long t0 = clock64();
+            mbar_wait(&full[stage], phase);
+            const long long t1 = clock64();
+            wait_cycles += t1 - t0;
+            if (blockIdx.x == 0 && it < 16 && kb < 256) p.trace[65536 + (it * 256 + kb) * 2 + 1] = t1;
+          } else {
+            mbar_wait(&full[stage], phase);
+          }
+          tc_fence_after();
+          issue(0, stage, kb);
+          if constexpr (C::MSUB == 1) {
+            tc_commit_mc(&empty[stage], all_ctas);  // every CTA of the cluster
+          } else if (sub1_ready) {
+            issue(1, stage, kb);
+            tc_commit_mc(&empty[stage], all_ctas);
+          } else {
+            if (lag++ == 0) {
+              lag_stage = stage;
+              lag_kb = kb;
+            }
+            // catch up once subtile 1 is drained; block when the ring is
+            // exhausted or the tile's k-loop ends
+            if (lag == C::STAGES || kb == p.num_kb - 1 || mbar_test(&tempty[1], acc_phase ^ 1)) {
               mbar_wait(&tempty[1], acc_phase ^ 1);
               tc_fence_after();
-            }
-#pragma unroll
-            for (int j = 0; j < C::MMAS; ++j) {
-              const uint32_t acc_flag = (kb | j) != 0;
-              const uint64_t adesc = smem_desc(a_base + h * C::A_SUB + j * 32, 16, 1024, 2);
-              const uint32_t d = d_tmem + h * C::ACC_COLS;
-              if constexpr (C::SPARSE) {
-                const uint64_t bdesc = smem_desc(b_base + (j >> 1) * C::B_ATOM + (j & 1) * 64, 16, 1024, 2);
-                umma_sparse_cg2<C::KIND>(d, adesc, bdesc, tmem + C::E_COL + 8 * h + 2 * j, C::IDESC, acc_flag);
-              } else {
-                const uint64_t bdesc = smem_desc(b_base + j * 32, 16, 1024, 2);
-                umma_dense_cg2<C::KIND>(d, adesc, bdesc, C::IDESC, acc_flag);
+              SLSP_TRACE(it, 1);
+              sub1_ready = true;
+              int st = lag_stage;
+              for (int i = 0; i < lag; ++i) {
+                issue(1, st, lag_kb + i);
+                tc_commit_mc(&empty[st], all_ctas);
+                if (++st == C::STAGES) st = 0;
               }
+              lag = 0;
             }
           }
-          tc_commit_mc(&empty[stage], static_cast<uint16_t>((1u << C::CL) - 1));  // every CTA of the cluster
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
+        SLSP_TRACE(it, 2);
+        if (p.trace && blockIdx.x == 0) p.trace[it * 16 + 8] = wait_cycles;
         tc_commit_mc(&tfull[acc], static_cast<uint16_t>(0x3u << lead));  // this pair's epilogues
       }
+    }
+  } else if constexpr (C::REG_EPI) {
+    // ------------------------------------ register-staged epilogue ----
+    // 8 warps: two per TMEM lane quarter, each owning half of the tile's
+    // columns. Per subtile: tcgen05.ld (software-pipelined, 16 columns at a
+    // time) -> dequant -> BF16 pairs in registers -> release the subtile's
+    // TMEM to the MMA warp. Stores (32 B per lane) come after both releases
+    // when the two subtiles fit in registers (BN <= 224), else per subtile.
+    // Scales are fetched before the accumulator wait: s_ch into registers,
+    // the warp's s_tok slice into a warp-private smem slice (LDS.128 broadcast).
+    const uint32_t quarter = warp & 3;
+    const uint32_t half = (warp - 2) >> 2;
+    const uint32_t lane = lane_id();
+    const uint64_t pol = (p.hints & kHintOutFirst) ? policy_evict_first() : policy_evict_normal();
+    float* stok_sm = reinterpret_cast<float*>(smem + C::OFF_EPI + (warp - 2) * C::EPI_WARP);
+    constexpr int HALF = C::BN / 2;
+    constexpr bool HOLD_BOTH = C::REG_CHUNKS <= 7;
+    int it = 0;
+    for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
+      int ms, nt;
+      tile_coords(tile, p, m_super, ms, nt);
+      const int mt = ms * C::NPAIR + static_cast<int>(pair);
+      const int64_t tcol0 = static_cast<int64_t>(nt) * C::BN + half * HALF;
+      const int64_t row0 = static_cast<int64_t>(mt) * C::BM + rank * C::A_ROWS + quarter * 32 + lane;
+      const float sc0 = row0 < p.n ? __ldg(p.s_ch + row0) : 0.f;
+      const float sc1 = row0 + 256 < p.n ? __ldg(p.s_ch + row0 + 256) : 0.f;
+#pragma unroll
+      for (int i = static_cast<int>(lane); i < HALF; i += 32)
+        stok_sm[i] = tcol0 + i < p.m ? __ldg(p.s_tok + tcol0 + i) : 0.f;
+      __syncwarp();
+      mbar_wait(&tfull[0], it & 1);
+      tc_fence_after();
+      if (warp == 2 && lane == 0) SLSP_TRACE(it, 3);
+
+      auto drain = [&](int h, float sc, uint32_t (&pk)[C::REG_CHUNKS][8]) {
+        const uint32_t t_base = tmem + ((quarter * 32) << 16) + h * C::ACC_COLS + half * HALF;
+        uint32_t r[2][16];
+        tmem_ld_32x32b_x16(t_base, r[0]);
+        tmem_ld_wait_regs(r[0]);
+#pragma unroll
+        for (int c = 0; c < C::REG_CHUNKS; ++c) {
+          if (c + 1 < C::REG_CHUNKS) tmem_ld_32x32b_x16(t_base + (c + 1) * 16, r[(c + 1) & 1]);
+          dequant16_smem<typename C::Acc>(r[c & 1], sc, smem_u32(stok_sm) + c * 64, pk[c]);
+          reg_pin(pk[c]);  // keep the math before the TMEM release (no sinking into the stores)
+          if (c + 1 < C::REG_CHUNKS) tmem_ld_wait_regs(r[(c + 1) & 1]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[h]), lead));
+        if (warp == 2 && lane == 0) SLSP_TRACE(it, 4 + 2 * h);
+      };
+      auto store = [&](int h, const uint32_t (&pk)[C::REG_CHUNKS][8]) {
+        const int64_t row = row0 + h * 256;
+        if ((p.debug & kDbgNoStore) || row >= p.n) return;
+        uint8_t* dst_row = reinterpret_cast<uint8_t*>(p.out) + (row * p.ldo + tcol0) * 2;
+        if (p.direct_vec == 2 && tcol0 + HALF <= p.m) {
+#pragma unroll
+          for (int c = 0; c < C::REG_CHUNKS; ++c) {
+            st_global_v8_hint(dst_row + c * 32, pk[c], pol);
+            if (p.store_gap_ns) __nanosleep(p.store_gap_ns);  // pace the output stream under the next mainloop
+          }
+        } else {  // token tail or unaligned rows: element stores from a local copy (cold path)
+          uint32_t tmp[C::REG_CHUNKS * 8];
+#pragma unroll
+          for (int c = 0; c < C::REG_CHUNKS; ++c)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) tmp[c * 8 + i] = pk[c][i];
+          store_tail_u16(reinterpret_cast<uint16_t*>(dst_row), tmp, static_cast<int>(imin64(HALF, p.m - tcol0)));
+        }
+      };
+      if constexpr (HOLD_BOTH) {
+        uint32_t pk0[C::REG_CHUNKS][8], pk1[C::REG_CHUNKS][8];
+        drain(0, sc0, pk0);
+        drain(1, sc1, pk1);
+        store(0, pk0);
+        if (warp == 2 && lane == 0) SLSP_TRACE(it, 5);
+        store(1, pk1);
+      } else {
+        uint32_t pk[C::REG_CHUNKS][8];
+        drain(0, sc0, pk);
+        store(0, pk);
+        if (warp == 2 && lane == 0) SLSP_TRACE(it, 5);
+        drain(1, sc1, pk);
+        store(1, pk);
+      }
+      if (warp == 2 && lane == 0) SLSP_TRACE(it, 7);
     }
   } else {
     // ------------------------------------------------ epilogue ----
@@ -487,17 +725,25 @@ uint32_t env_knob(const char* name, uint32_t dflt) {
   return (e && *e) ? static_cast<uint32_t>(std::strtoul(e, nullptr, 0)) : dflt;
 }
 
-// Byte-addressed 2D map (uint8 elements): rows x row_bytes, box rows x 128 B, 128B swizzle.
-int make_map_2d(CUtensorMap* map, const void* base, uint64_t row_bytes, uint64_t rows, uint32_t box_rows) {
+uintptr_t env_ptr(const char* name) {
+  const char* e = std::getenv(name);
+  return (e && *e) ? static_cast<uintptr_t>(std::strtoull(e, nullptr, 0)) : 0;
+}
+
+// Byte-addressed 2D map (uint8 elements): rows x row_bytes, box rows x box_bytes
+// (128 B: 128B swizzle, 64 B: 64B swizzle).
+int make_map_2d(CUtensorMap* map, const void* base, uint64_t row_bytes, uint64_t rows, uint32_t box_rows,
+                uint32_t box_bytes = 128) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return SLSP_ERR_CUDA;
   cuuint64_t dims[2] = {row_bytes, rows};
   cuuint64_t strides[1] = {row_bytes};
-  cuuint32_t box[2] = {128, box_rows};
+  cuuint32_t box[2] = {box_bytes, box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   box_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? SLSP_OK : SLSP_ERR_CUDA;
 }
 
@@ -505,13 +751,13 @@ int make_map_2d(CUtensorMap* map, const void* base, uint64_t row_bytes, uint64_t
 // 256-byte rows; one box {256, 16} is the contiguous 4 KB block of a stage
 // (two canonical 128x16B tcgen05.cp atoms) — 16 wide requests instead of 256
 // 16-byte ones.
-int make_map_meta(CUtensorMap* map, const void* base, uint64_t rows, uint64_t kp) {
+int make_map_meta(CUtensorMap* map, const void* base, uint64_t rows, uint64_t kp, uint32_t box_rows = 16) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return SLSP_ERR_CUDA;
   const uint64_t bytes = static_cast<uint64_t>(slsp_tiled_meta_bytes(static_cast<int64_t>(rows), static_cast<int64_t>(kp)));
   cuuint64_t dims[2] = {256, bytes / 256};
   cuuint64_t strides[1] = {256};
-  cuuint32_t box[2] = {256, 16};
+  cuuint32_t box[2] = {256, box_rows};  // 16: a 256-wide k-stage, 8: a half stage
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -550,13 +796,17 @@ int make_map_out(CUtensorMap* map, void* base, int out_mode, int64_t n, int64_t 
 // Epilogue store path: TMA staging (1) or direct 16-byte vector stores (2);
 // env SLSP_GEMM_EPI overrides the default (0 = auto: vectors for the
 // 2-subtile tiles' narrow chunks, TMA otherwise). MN output always uses TMA.
-void select_epilogue(Params& p, int out_mode, uint32_t msub) {
+void select_epilogue(Params& p, int out_mode, uint32_t msub, const void* out, int64_t ldo, const float* s_tok) {
   const uint32_t epi = env_knob("SLSP_GEMM_EPI", 0);
+  const int esz = out_mode == SLSP_OUT_RAW_NM ? 4 : 2;
+  const uintptr_t base = reinterpret_cast<uintptr_t>(out);
+  const int64_t row_bytes = ldo * esz;
+  p.direct_vec = (base % 32 == 0 && row_bytes % 32 == 0) ? 2 : (base % 16 == 0 && row_bytes % 16 == 0) ? 1 : 0;
+  p.stok_vec = (reinterpret_cast<uintptr_t>(s_tok) % 16) == 0;
+  // MSUB=2 BF16 [N][M] uses the register-staged epilogue (direct stores);
+  // otherwise TMA staging where rows are 16-byte aligned, unless overridden
   const bool aligned = p.tma_store != 0;  // make_map_out enables TMA iff rows are 16-byte aligned
-  if (out_mode != SLSP_OUT_BF16_MN && aligned && (epi == 2 || (epi == 0 && msub == 2))) {
-    p.tma_store = 0;
-    p.direct_vec = 1;
-  }
+  if (out_mode != SLSP_OUT_BF16_MN && aligned && (epi == 2 || (epi == 0 && msub == 2))) p.tma_store = 0;
 }
 
 int num_sms() {
@@ -605,44 +855,60 @@ int run(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const 
   return SLSP_OK;
 }
 
-// Pipeline depth that fits 227 KB of smem for each configuration.
-constexpr int stages_for(bool sparse, int msub, bool raw) {
-  if (msub == 1) return sparse ? 4 : 6;
-  return sparse ? (raw ? 2 : 3) : (raw ? 3 : 4);
-}
-
-template <bool SPARSE, MmaKind K, int BN, int CL, int MSUB>
+template <bool SPARSE, MmaKind K, int BN, int CL, int MSUB, int KH>
 int run_out_cl(int out_mode, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const CUtensorMap& o,
                const Params& p, cudaStream_t s) {
-  constexpr int SR = stages_for(SPARSE, MSUB, true), SB = stages_for(SPARSE, MSUB, false);
-  switch (out_mode) {
-    case SLSP_OUT_RAW_NM: return run<Cfg<SPARSE, K, BN, SR, SLSP_OUT_RAW_NM, CL, MSUB>>(a, b, e, o, p, s);
-    case SLSP_OUT_BF16_NM: return run<Cfg<SPARSE, K, BN, SB, SLSP_OUT_BF16_NM, CL, MSUB>>(a, b, e, o, p, s);
-    case SLSP_OUT_BF16_MN: return run<Cfg<SPARSE, K, BN, SB, SLSP_OUT_BF16_MN, CL, MSUB>>(a, b, e, o, p, s);
+  switch (out_mode) {  // STAGES = 0: as many as fit
+    case SLSP_OUT_RAW_NM: return run<Cfg<SPARSE, K, BN, 0, SLSP_OUT_RAW_NM, CL, MSUB, KH>>(a, b, e, o, p, s);
+    case SLSP_OUT_BF16_NM: return run<Cfg<SPARSE, K, BN, 0, SLSP_OUT_BF16_NM, CL, MSUB, KH>>(a, b, e, o, p, s);
+    case SLSP_OUT_BF16_MN: return run<Cfg<SPARSE, K, BN, 0, SLSP_OUT_BF16_MN, CL, MSUB, KH>>(a, b, e, o, p, s);
   }
   return SLSP_ERR_INVALID;
 }
 
 // Tile shape knobs: cluster 2 (one CTA pair) or 4 (two pairs sharing
-// activation tiles by TMA multicast), and 1 or 2 M-subtiles per pair; env
-// SLSP_GEMM_CLUSTER / SLSP_GEMM_MSUB override the per-kernel defaults.
+// activation tiles by TMA multicast), 1 or 2 M-subtiles per pair, and (sparse)
+// half k-stages; env SLSP_GEMM_CLUSTER / SLSP_GEMM_MSUB / SLSP_GEMM_KHALF
+// override the per-kernel defaults.
+template <bool SPARSE, MmaKind K, int BN, int KH>
+int run_out_kh(int out_mode, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const CUtensorMap& o,
+               const Params& p, cudaStream_t s, uint32_t cluster, uint32_t msub) {
+  if (cluster == 4)
+    return msub == 2 ? run_out_cl<SPARSE, K, BN, 4, 2, KH>(out_mode, a, b, e, o, p, s)
+                     : run_out_cl<SPARSE, K, BN, 4, 1, KH>(out_mode, a, b, e, o, p, s);
+  return msub == 2 ? run_out_cl<SPARSE, K, BN, 2, 2, KH>(out_mode, a, b, e, o, p, s)
+                   : run_out_cl<SPARSE, K, BN, 2, 1, KH>(out_mode, a, b, e, o, p, s);
+}
+
 template <bool SPARSE, MmaKind K, int BN>
 int run_out(int out_mode, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const CUtensorMap& o,
-            const Params& p, cudaStream_t s, uint32_t cluster, uint32_t msub) {
-  if (cluster == 4)
-    return msub == 2 ? run_out_cl<SPARSE, K, BN, 4, 2>(out_mode, a, b, e, o, p, s)
-                     : run_out_cl<SPARSE, K, BN, 4, 1>(out_mode, a, b, e, o, p, s);
-  return msub == 2 ? run_out_cl<SPARSE, K, BN, 2, 2>(out_mode, a, b, e, o, p, s)
-                   : run_out_cl<SPARSE, K, BN, 2, 1>(out_mode, a, b, e, o, p, s);
+            const Params& p, cudaStream_t s, uint32_t cluster, uint32_t msub, uint32_t kh) {
+  if constexpr (SPARSE)
+    if (kh) return run_out_kh<SPARSE, K, BN, 1>(out_mode, a, b, e, o, p, s, cluster, msub);
+  return run_out_kh<SPARSE, K, BN, 0>(out_mode, a, b, e, o, p, s, cluster, msub);
 }
 
 constexpr int kSparseBN = 224;
 constexpr int kDenseBN = 256;
 constexpr uint32_t kSparseCluster = 2;
 constexpr uint32_t kDenseCluster = 2;
-constexpr uint32_t kSparseMsub = 1;
 constexpr uint32_t kDenseMsub = 1;
+constexpr uint32_t kSparseKHalf = 0;
+constexpr uint32_t kStoreGapNs = 0;
 constexpr uint32_t kRasterGroup = 16;  // measured best of {4, 8, 16, 32, 148} on Qwen2.5-7B shapes
+
+// M-subtiles for the sparse kernel: two subtiles (512 weight rows per pair,
+// activation tile shared) move 29% fewer operand bytes per MAC but halve the
+// tile count; use them unless that leaves a partial last wave the one-subtile
+// grid would not have (measured on Qwen2.5-7B shapes).
+uint32_t sparse_msub(int64_t n, int64_t m, uint32_t cluster) {
+  const int64_t clusters = num_sms() / static_cast<int64_t>(cluster);
+  const int64_t nt = (m + kSparseBN - 1) / kSparseBN;
+  const int64_t t1 = (n + 255) / 256 * nt, t2 = (n + 511) / 512 * nt;
+  const int64_t w1 = (t1 + clusters - 1) / clusters, w2 = (t2 + clusters - 1) / clusters;
+  // per-tile cost of a 2-subtile tile ~ 1.9x a 1-subtile tile
+  return 19 * w2 <= 10 * w1 ? 2u : 1u;
+}
 
 int check_out(int out_mode, const float* s_ch, const float* s_tok, void* out, int64_t ldo, int64_t n, int64_t m) {
   if (!out) return SLSP_ERR_INVALID;
@@ -677,28 +943,31 @@ int slsp_sparse_gemm(int dtype, const void* values, const uint8_t* meta, int64_t
   if (n == 0 || m == 0) return SLSP_OK;
   CUtensorMap ta, tb, te, to;
   Params p{};
-  if ((st = make_map_2d(&ta, values, kp / 2, n, 128))) return st;
+  const uint32_t kh = env_knob("SLSP_GEMM_KHALF", kSparseKHalf) ? 1 : 0;
+  if ((st = make_map_2d(&ta, values, kp / 2, n, 128, kh ? 64 : 128))) return st;
   // activation box: the CTA's half of the N tile, split once more across the
   // pairs of a 4-CTA cluster (each pair fetches one slice and multicasts it)
   const uint32_t cluster = env_knob("SLSP_GEMM_CLUSTER", kSparseCluster) == 4 ? 4 : 2;
-  const uint32_t msub = env_knob("SLSP_GEMM_MSUB", kSparseMsub) == 2 ? 2 : 1;
+  const uint32_t msub = env_knob("SLSP_GEMM_MSUB", sparse_msub(n, m, cluster)) == 2 ? 2 : 1;
   if ((st = make_map_2d(&tb, act, kp, m, kSparseBN / 2 / (cluster / 2)))) return st;
-  if ((st = make_map_meta(&te, meta, n, kp))) return st;
+  if ((st = make_map_meta(&te, meta, n, kp, kh ? 8 : 16))) return st;
   if ((st = make_map_out(&to, out, out_mode, n, m, ldo, msub == 2 ? 16 : 32, &p.tma_store))) return st;
-  select_epilogue(p, out_mode, msub);
+  select_epilogue(p, out_mode, msub, out, ldo, s_tok);
   p.n = n;
   p.m = m;
-  p.num_kb = static_cast<int>(kp / 256);
+  p.num_kb = static_cast<int>(kp / (kh ? 128 : 256));
   p.s_ch = s_ch;
   p.s_tok = s_tok;
   p.out = out;
   p.ldo = ldo;
   p.debug = debug_flags();
+  p.trace = reinterpret_cast<unsigned long long*>(env_ptr("SLSP_GEMM_TRACE"));
+  p.store_gap_ns = env_knob("SLSP_GEMM_STORE_GAP", kStoreGapNs);
   p.hints = env_knob("SLSP_GEMM_HINTS", kDefaultHints);
   p.group = static_cast<int>(env_knob("SLSP_GEMM_GROUP", kRasterGroup));
   if (dtype == SLSP_DT_I8)
-    return run_out<true, MmaKind::I8, kSparseBN>(out_mode, ta, tb, te, to, p, s, cluster, msub);
-  return run_out<true, MmaKind::F8, kSparseBN>(out_mode, ta, tb, te, to, p, s, cluster, msub);
+    return run_out<true, MmaKind::I8, kSparseBN>(out_mode, ta, tb, te, to, p, s, cluster, msub, kh);
+  return run_out<true, MmaKind::F8, kSparseBN>(out_mode, ta, tb, te, to, p, s, cluster, msub, kh);
 }
 
 int slsp_dense_gemm(int dtype, const void* w, int64_t n, int64_t k, const void* act, int64_t m, const float* s_ch,
@@ -722,7 +991,7 @@ int slsp_dense_gemm(int dtype, const void* w, int64_t n, int64_t k, const void* 
   const uint32_t msub = env_knob("SLSP_GEMM_MSUB", kDenseMsub) == 2 ? 2 : 1;
   if ((st = make_map_2d(&tb, act, k * esz, m, kDenseBN / 2 / (cluster / 2)))) return st;
   if ((st = make_map_out(&to, out, out_mode, n, m, ldo, msub == 2 ? 16 : 32, &p.tma_store))) return st;
-  select_epilogue(p, out_mode, msub);
+  select_epilogue(p, out_mode, msub, out, ldo, s_tok);
   p.n = n;
   p.m = m;
   p.num_kb = static_cast<int>(k * esz / 128);
@@ -731,13 +1000,15 @@ int slsp_dense_gemm(int dtype, const void* w, int64_t n, int64_t k, const void* 
   p.out = out;
   p.ldo = ldo;
   p.debug = debug_flags();
+  p.trace = reinterpret_cast<unsigned long long*>(env_ptr("SLSP_GEMM_TRACE"));
+  p.store_gap_ns = env_knob("SLSP_GEMM_STORE_GAP", kStoreGapNs);
   p.hints = env_knob("SLSP_GEMM_HINTS", kDefaultHints);
   p.group = static_cast<int>(env_knob("SLSP_GEMM_GROUP", kRasterGroup));
   if (dtype == SLSP_DT_I8)
-    return run_out<false, MmaKind::I8, kDenseBN>(out_mode, ta, tb, ta, to, p, s, cluster, msub);
+    return run_out<false, MmaKind::I8, kDenseBN>(out_mode, ta, tb, ta, to, p, s, cluster, msub, 0);
   if (dtype == SLSP_DT_E4M3)
-    return run_out<false, MmaKind::F8, kDenseBN>(out_mode, ta, tb, ta, to, p, s, cluster, msub);
-  return run_out<false, MmaKind::F16, kDenseBN>(out_mode, ta, tb, ta, to, p, s, cluster, msub);
+    return run_out<false, MmaKind::F8, kDenseBN>(out_mode, ta, tb, ta, to, p, s, cluster, msub, 0);
+  return run_out<false, MmaKind::F16, kDenseBN>(out_mode, ta, tb, ta, to, p, s, cluster, msub, 0);
 }
 
 }  // extern "C"
