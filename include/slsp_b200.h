@@ -159,6 +159,31 @@ SLSP_API int slsp_sparse_gemm(int dtype, const void* values, const uint8_t* meta
                      int64_t m, const float* s_ch, const float* s_tok, int out_mode, void* out, int64_t ldo,
                      slsp_stream_t stream);
 
+/* GEMM window order for in-SM lifting (6:8). Permutes the windows of
+ * slsp_pack_compress output (values rows x kp_ref/2, row-major codes
+ * rows x kp_ref/8; K' = 3*ceil(cols/8)*4 real lifted positions) into the
+ * order slsp_sparse_gemm_x consumes: per period of 64 source blocks (512
+ * source bytes), the 128 windows (block b: window 0, window 2) for b = 0..63,
+ * then the 64 windows 1. Output width kp_out = 3/2 * round_up(cols, 512);
+ * blocks past the real ones are padding windows (values 0, codes (0,1)).
+ * values_out: rows x kp_out/2, codes_out: rows x kp_out/8 (row-major, to be
+ * tiled with slsp_tile_meta(codes_out, rows, kp_out, ...)). The sum over the
+ * lifted dimension is order-independent, so slsp_sparse_gemm_x reproduces
+ * slsp_sparse_gemm (== gemm.hpp:199-233) bit for bit. */
+SLSP_API int slsp_gemm_order(int dtype, const void* values, const uint8_t* codes, int64_t rows, int64_t cols, int64_t kp_ref,
+                    void* values_out, uint8_t* codes_out, int64_t kp_out, slsp_stream_t stream);
+
+/* Sparse GEMM with in-SM activation lifting (6:8). act is the UNLIFTED
+ * quantized activation (slsp_quantize_rows output, m x kx bytes, kx =
+ * round_up(cols, 512), zero padded); values/meta from slsp_gemm_order +
+ * slsp_tile_meta with kp = 3*kx/2. The window-duplicating rearrangement of
+ * fused_quant_slide (quantize.hpp:122-174) happens in shared memory inside
+ * the GEMM. Results equal slsp_sparse_gemm on fused_quant_slide's payload
+ * bit for bit (int32) / to the same fp32 epilogue (BF16). */
+SLSP_API int slsp_sparse_gemm_x(int dtype, const void* values, const uint8_t* meta, int64_t n, int64_t kx, const void* act,
+                       int64_t m, const float* s_ch, const float* s_tok, int out_mode, void* out, int64_t ldo,
+                       slsp_stream_t stream);
+
 /* a15 — gemm.hpp:142-162 dense_gemm on tcgen05.mma (the speedup
  * denominator). w: n x k, act: m x k (token rows; the reference's X is k x m,
  * the C++ shim transposes), k % 128 == 0. Outputs as slsp_sparse_gemm. */

@@ -9,13 +9,14 @@ or a B200 is missing, calls raise.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from dataclasses import dataclass
 from pathlib import Path
 
 import torch
 
-LIB_PATH = Path(__file__).resolve().parent / "libslsp_b200.so"
+LIB_PATH = Path(os.environ.get("SLSP_LIB") or Path(__file__).resolve().parent / "libslsp_b200.so")
 
 # ---- constants mirrored from include/slsp_b200.h -----------------------------
 DT_I8, DT_BF16, DT_E4M3, DT_F32, DT_F64 = 0, 1, 2, 3, 4
@@ -102,6 +103,8 @@ def lib() -> C.CDLL:
                 "slsp_sparse_gemm": (i32, [i32, vp, vp, i64, i64, vp, i64, vp, vp, i32, vp, i64, vp]),
                 "slsp_dense_gemm": (i32, [i32, vp, i64, i64, vp, i64, vp, vp, i32, vp, i64, vp]),
                 "slsp_tile_meta": (i32, [vp, i64, i64, vp, vp]),
+                "slsp_gemm_order": (i32, [i32, vp, vp, i64, i64, i64, vp, vp, i64, vp]),
+                "slsp_sparse_gemm_x": (i32, [i32, vp, vp, i64, i64, vp, i64, vp, vp, i32, vp, i64, vp]),
                 "slsp_tiled_meta_bytes": (i64, [i64, i64]),
             }
             for name, (res, args) in sigs.items():
@@ -229,6 +232,41 @@ class PackedWeights:
             self.meta_tiled = tile_meta(self.meta, self.n, self.kp)
         return self.meta_tiled
 
+    def gemm_order(self) -> "GemmOrderWeights":
+        """The in-SM-lifting operand (slsp_gemm_order + slsp_tile_meta), built once."""
+        if getattr(self, "_gemm_order", None) is None:
+            self._gemm_order = gemm_order(self)
+        return self._gemm_order
+
+
+@dataclass
+class GemmOrderWeights:
+    """Weights in the window order of slsp_sparse_gemm_x (6:8): values n x kp/2,
+    tiled metadata; kx = round_up(k, 512) activation bytes per token, kp = 3kx/2."""
+    values: torch.Tensor
+    meta_tiled: torch.Tensor
+    n: int
+    k: int
+    kx: int
+    kp: int
+
+    @property
+    def dtype(self) -> int:
+        return dtype_code(self.values)
+
+
+def gemm_order(w: PackedWeights) -> GemmOrderWeights:
+    """slsp_gemm_order: reference window order -> the in-SM-lifting GEMM order (6:8 only)."""
+    if (w.z, w.l) != (6, 8):
+        raise UnsupportedError("in-SM lifting is implemented for the 6:8 pattern")
+    kx = round_up(w.k, 512)
+    kp = kx * 3 // 2
+    values = torch.empty((w.n, kp // 2), dtype=w.values.dtype, device=w.values.device)
+    codes = torch.empty((w.n, kp // 8), dtype=torch.uint8, device=w.values.device)
+    _check(lib().slsp_gemm_order(w.dtype, _ptr(_raw(w.values)), _ptr(w.meta), w.n, w.k, w.kp, _ptr(_raw(values)),
+                                 _ptr(codes), kp, _stream(values.device)), "gemm_order")
+    return GemmOrderWeights(values, tile_meta(codes, w.n, kp), w.n, w.k, kx, kp)
+
 
 def tile_meta(meta: torch.Tensor, rows: int, kp: int) -> torch.Tensor:
     """Row-major codes -> the MMA-tiled metadata layout (slsp_tile_meta)."""
@@ -352,6 +390,24 @@ def sparse_gemm(w: PackedWeights, act: torch.Tensor, s_ch: torch.Tensor | None =
     ldo = o.shape[1]
     _check(lib().slsp_sparse_gemm(w.dtype, _ptr(_raw(w.values)), _ptr(w.tiled()), w.n, w.kp, _ptr(act), m, _ptr(s_ch),
                                   _ptr(s_tok), out_mode, _ptr(o), ldo, _stream(act.device)), "sparse_gemm")
+    return o
+
+
+def sparse_gemm_x(w: "PackedWeights | GemmOrderWeights", act: torch.Tensor, s_ch: torch.Tensor | None = None,
+                  s_tok: torch.Tensor | None = None, out_mode: int = OUT_RAW_NM,
+                  out: torch.Tensor | None = None) -> torch.Tensor:
+    """Sparse GEMM with in-SM lifting: act = quantize_rows(x, kpad=w.kx) (m x kx
+    bytes, UNLIFTED); equals sparse_gemm(w, fused_quant_slide(x)) bit for bit."""
+    g = w.gemm_order() if isinstance(w, PackedWeights) else w
+    _require_cuda(act, s_ch, s_tok)
+    m = act.shape[0]
+    if act.shape[1] * act.element_size() != g.kx:
+        raise DimensionMismatchError(f"activation rows must be kx = {g.kx} bytes (quantize_rows(x, kpad=kx))")
+    o = _gemm_out(out_mode, g.n, m, g.values.dtype == torch.int8, act.device, out)
+    ldo = o.shape[1]
+    _check(lib().slsp_sparse_gemm_x(g.dtype, _ptr(_raw(g.values)), _ptr(g.meta_tiled), g.n, g.kx, _ptr(act), m,
+                                    _ptr(s_ch), _ptr(s_tok), out_mode, _ptr(o), ldo, _stream(act.device)),
+           "sparse_gemm_x")
     return o
 
 

@@ -52,6 +52,17 @@ def _stale() -> bool:
     return STAMP.read_text().strip() != _digest()
 
 
+def build_watchdog() -> Path:
+    """Debug variant libslsp_b200_wd.so (-DSLSP_WATCHDOG: stuck mbarrier waits
+    print and trap); load it with SLSP_LIB=<path>. Never used by the product."""
+    out = PKG / "libslsp_b200_wd.so"
+    srcs = [str(CSRC / s) for s in SOURCES]
+    cmd = [NVCC, *[f for f in FLAGS if f not in ("-cudart", "static")], "-cudart", "static", "-DSLSP_WATCHDOG",
+           *srcs, "-o", str(out)]
+    subprocess.run(cmd, check=True)
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not _stale():
         return LIB
@@ -85,5 +96,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 
 
 if __name__ == "__main__":
+    if "--watchdog" in sys.argv:
+        print(build_watchdog())
+        sys.exit(0)
     build(force="--force" in sys.argv, verbose=True)
     print(LIB)

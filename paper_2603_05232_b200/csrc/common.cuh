@@ -2,6 +2,7 @@
 // small numeric utilities. Inline PTX only; no CUTLASS/CuTe dispatch.
 #pragma once
 
+#include <cstdio>
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -72,6 +73,34 @@ SLSP_DEVINL void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 
+// Release at cluster scope: orders this thread's prior shared-memory writes
+// (already fenced to the async proxy) before the remote barrier's completion.
+SLSP_DEVINL void mbar_arrive_release_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+#ifdef SLSP_WATCHDOG
+// Debug build (build.py --watchdog): a wait that spins ~seconds reports the
+// barrier (smem offset, parity) of the first stuck thread and traps.
+SLSP_DEVINL void mbar_wait(uint64_t* bar, uint32_t parity) {
+  for (long long n = 0;; ++n) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (n == (1ll << 21)) {
+      printf("SLSP WATCHDOG block %d warp %d lane %d: barrier smem+%u parity %u\n", blockIdx.x, threadIdx.x / 32,
+             threadIdx.x % 32, smem_u32(bar), parity);
+      asm volatile("trap;");
+    }
+  }
+}
+#else
 SLSP_DEVINL void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n"
@@ -83,6 +112,7 @@ SLSP_DEVINL void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+#endif
 
 SLSP_DEVINL void mbar_wait_cluster_acquire(uint64_t* bar, uint32_t parity) {
   asm volatile(
@@ -128,6 +158,15 @@ SLSP_DEVINL void tma_load_2d_cg2_hint(void* dst, const CUtensorMap* map, uint32_
       "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
       " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
+}
+
+// Plain (one-CTA) tensor load into this CTA's smem, completion on a local barrier.
+SLSP_DEVINL void tma_load_2d_hint(void* dst, const CUtensorMap* map, uint32_t bar, int c0, int c1, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "l"(policy)
       : "memory");
 }
 
@@ -317,8 +356,14 @@ SLSP_DEVINL void tmem_ld_32x32b_x16(uint32_t taddr, uint32_t (&r)[16]) {
 
 template <int N>
 SLSP_DEVINL void tmem_ld_cols(uint32_t taddr, uint32_t (&r)[N]) {
-  if constexpr (N == 32) tmem_ld_32x32b_x32(taddr, r);
-  else tmem_ld_32x32b_x16(taddr, r);
+  if constexpr (N == 64) {
+    tmem_ld_32x32b_x32(taddr, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+    tmem_ld_32x32b_x32(taddr + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+  } else if constexpr (N == 32) {
+    tmem_ld_32x32b_x32(taddr, r);
+  } else {
+    tmem_ld_32x32b_x16(taddr, r);
+  }
 }
 
 SLSP_DEVINL void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
@@ -332,6 +377,12 @@ SLSP_DEVINL void tmem_ld_wait_regs(uint32_t (&r)[16]) {
                  "+r"(r[15])
                :
                : "memory");
+}
+
+SLSP_DEVINL uint4 ld_shared_u4(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
 }
 
 SLSP_DEVINL float4 ld_shared_f4(uint32_t addr) {

@@ -35,55 +35,67 @@ constexpr int kNumThreads = 192;
 // bit1 skip operand loads (MMA on stale smem), bit2 load k-block 0 of tile 0
 // only (L2-resident operands), bit3 skip metadata loads, bit4 skip the MMAs
 // (load pipeline alone). Results are garbage when set; perf probing only.
-enum : uint32_t { kDbgNoStore = 1u, kDbgNoLoad = 2u, kDbgSameTile = 4u, kDbgNoMeta = 8u, kDbgNoMma = 16u };
+// bit5 skips the activation (B) load of every third k-block (in-SM lifting
+// emulation: the L2 traffic of a kernel that builds those stages in smem).
+// bit6 (LIFT) skips the C-block build, bit7 (LIFT) skips its proxy fence.
+enum : uint32_t { kDbgNoStore = 1u, kDbgNoLoad = 2u, kDbgSameTile = 4u, kDbgNoMeta = 8u, kDbgNoMma = 16u,
+                  kDbgSkipB3 = 32u, kDbgNoBuild = 64u, kDbgNoFence = 128u };
 // L2 cache-policy hints (env SLSP_GEMM_HINTS overrides kDefaultHints).
 enum : uint32_t { kHintBLast = 1u, kHintAFirst = 2u, kHintOutFirst = 4u };
 constexpr uint32_t kDefaultHints = kHintBLast | kHintOutFirst;
 
-template <bool SPARSE_, MmaKind KIND_, int BN_, int STAGES_, int OUT_, int CL_ = 2, int MSUB_ = 1, int KH_ = 0>
+// Epilogue chunk width (columns per tcgen05.ld + TMA store box).
+constexpr int epi_cols(int msub, int bn, int out) {
+  // msub 2: the register-staged BF16 [N][M] epilogue stores 32-column boxes;
+  // the generic path drains 16-column chunks
+  return msub == 2 ? (out == SLSP_OUT_BF16_NM ? 32 : 16) : (out == SLSP_OUT_RAW_NM || bn % 64 != 0) ? 32 : 64;
+}
+
+template <bool SPARSE_, MmaKind KIND_, int BN_, int STAGES_, int OUT_, int MSUB_ = 1, int LIFT_ = 0, int EW_ = 0>
 struct Cfg {
   static constexpr bool SPARSE = SPARSE_;
   static constexpr MmaKind KIND = KIND_;
   static constexpr int BN = BN_;          // tokens per pair tile (MMA N)
   static constexpr int OUT = OUT_;
-  // Cluster: CL CTAs = CL/2 CTA pairs on adjacent weight tiles of the same
-  // token tile; with 2 pairs each activation (B) box is fetched once from L2
-  // and multicast to both pairs (each pair loads one half of every B box).
-  static constexpr int CL = CL_;
-  static constexpr int NPAIR = CL / 2;
-  static_assert(CL == 2 || CL == 4, "cluster of 1 or 2 CTA pairs");
+  static constexpr int CL = 2;            // one CTA pair per cluster
+  static constexpr int NPAIR = 1;
   // M-subtiles: the pair runs MSUB UMMAs (M=256 each) per k-step against the
   // same activation stage, so B traffic per MAC drops by MSUB. TMEM then holds
   // MSUB accumulators per tile; with MSUB=2 they are single-buffered and
   // 4*MSUB epilogue warps drain them in parallel.
   static constexpr int MSUB = MSUB_;
   static_assert(MSUB == 1 || MSUB == 2, "one or two M-subtiles per pair");
+  // In-SM lifting (sparse, (2N-2):2N with 8 | 2N... here 6:8): the activation
+  // operand arrives UNLIFTED (quantized X, K bytes per token) and the lifted
+  // K' is consumed in the GEMM window order of slsp_gemm_order: per 512
+  // source bytes, two "X" k-blocks whose B tile is X itself (windows 0 and 2
+  // of each 8-block are its bytes 0-3 and 4-7) and one "C" k-block holding
+  // window 1 (bytes 2-5) of those 64 blocks, which LIFT_WARPS build in shared
+  // memory from the two X tiles. The lifted activation never exists in HBM
+  // or L2, and a third of the B operand's L2->SM traffic disappears.
+  static constexpr bool LIFT = LIFT_ != 0;
+  static_assert(!LIFT || SPARSE, "in-SM lifting feeds the sparse kernel");
+  static constexpr int LIFT_WARPS = LIFT ? 2 : 0;
   static constexpr int ACC_STAGES = MSUB == 1 ? 2 : 1;
   static constexpr int EPI_WARPS = 4 * MSUB;
-  static constexpr int THREADS = 64 + 32 * EPI_WARPS;
+  static constexpr int THREADS = 64 + 32 * (EPI_WARPS + LIFT_WARPS);
   static constexpr int BM = 256 * MSUB;   // weight rows per pair tile
   static constexpr int A_ROWS = 128;      // per CTA per M-subtile
   static constexpr int B_ROWS = BN / 2;   // tokens per CTA
-  // Half k-stages (sparse only): 128 lifted bytes per stage instead of 256 —
-  // A rows of 64 B (64B swizzle), one B atom, one metadata atom, 2 MMAs —
-  // so twice as many, half-size stages keep more bytes in flight per SM.
-  static constexpr bool KH = KH_ != 0;
-  static_assert(!KH || SPARSE, "half k-stages are for the sparse kernel");
-  static constexpr int A_ROW = KH ? 64 : 128;                // A bytes per row per stage
-  static constexpr uint32_t A_LAYOUT = KH ? 4u : 2u;         // UMMA desc: SWIZZLE_64B / SWIZZLE_128B
+  static_assert(!LIFT || B_ROWS % (8 * (LIFT ? LIFT_WARPS : 1)) == 0, "lift warps own whole 8-row swizzle groups");
+  static constexpr int A_ROW = 128;                          // A bytes per row per stage
+  static constexpr uint32_t A_LAYOUT = 2u;                   // UMMA desc: SWIZZLE_128B
   static constexpr int A_SUB = 128 * A_ROW;                  // one swizzle-atom column of 128 rows
   static constexpr int A_STAGE = MSUB * A_SUB;
-  static constexpr int B_ATOMS = SPARSE && !KH ? 2 : 1;      // B bytes per stage = 2x A bytes for .sp
+  static constexpr int B_ATOMS = SPARSE ? 2 : 1;             // B bytes per stage = 2x A bytes for .sp
   static constexpr int B_ATOM = B_ROWS * 128;
   static constexpr int B_STAGE = B_ATOM * B_ATOMS;
-  static constexpr int B_PART = B_ROWS / NPAIR;  // rows of each B box one pair fetches (multicast)
-  static_assert(B_PART % 8 == 0, "multicast slices must be whole 128B-swizzle atoms");
-  static constexpr int E_ATOMS = KH ? 1 : 2;                 // 128x128b metadata atoms per stage and subtile
+  static constexpr int E_ATOMS = 2;                          // 128x128b metadata atoms per stage and subtile
   static constexpr int E_SUB = SPARSE ? E_ATOMS * 128 * 16 : 0;
   static constexpr int E_STAGE = MSUB * E_SUB;
   static constexpr int STAGE_TX = A_STAGE + B_STAGE + E_STAGE;
   static constexpr int K_BYTES_B = 128 * B_ATOMS;            // activation bytes consumed per stage
-  static constexpr int MMAS = KH ? 2 : 4;                    // k-steps per stage
+  static constexpr int MMAS = 4;                             // k-steps per stage
   static constexpr int ACC_COLS = BN;                        // 32-bit TMEM columns per accumulator
   static constexpr int E_COL = ACC_STAGES * MSUB * BN;       // metadata columns after the accumulators
   static constexpr int TMEM_COLS = 512;
@@ -93,27 +105,33 @@ struct Cfg {
   // epilogue: chunks of 32 rows x EPI_COLS columns, double-buffered smem
   // staging per warp (a TMA store reads one buffer while the next is filled)
   static constexpr int OUT_ESZ = OUT == SLSP_OUT_RAW_NM ? 4 : 2;
-  static constexpr int EPI_COLS = MSUB == 2 ? 16 : 32;
-  static constexpr int EPI_BUFS = 2;
+  // MSUB=1: 128-byte staging rows (64 BF16 / 32 int32 columns), so every TMA
+  // store writes whole 128-byte lines (measured: L2 write cost is per request)
+  static constexpr int EPI_COLS = EW_ ? EW_ : epi_cols(MSUB, BN, OUT);
+  // (LIFT with two subtiles: one staging buffer, so the ring keeps 3 stages)
+  static constexpr int EPI_BUFS = LIFT && MSUB == 2 ? 1 : 2;
   static constexpr int EPI_BUF = 32 * EPI_COLS * OUT_ESZ;
   static constexpr int EPI_ROW = EPI_COLS * OUT_ESZ;  // staging row bytes (NM layout) = swizzle span
   // MSUB=2 with BF16 [N][M] output: register-staged epilogue (each subtile is
   // dequantised into registers and its TMEM released before any store), no
   // smem staging.
   static constexpr bool REG_EPI = MSUB == 2 && OUT == SLSP_OUT_BF16_NM;
-  static constexpr int REG_CHUNKS = BN / 32;  // 16-column chunks per warp per subtile (half the columns)
-  static constexpr int EPI_WARP = REG_EPI ? (BN / 2) * 4 : EPI_BUFS * EPI_BUF;  // REG: s_tok slice
+  static constexpr int H0 = (BN / 2 + 31) / 32 * 32;  // REG: columns of the first warp of a lane quarter
+  // REG: s_tok slice + one 32x32 BF16 staging box per warp
+  static constexpr int EPI_WARP = REG_EPI ? H0 * 4 + 32 * 64 : EPI_BUFS * EPI_BUF;
   // smem ring depth: STAGES_ if given, else as many stages as fit (<= 8)
   static constexpr int FIXED_SMEM = EPI_WARPS * EPI_WARP + 4 * 8 + 16 + 1024;
   static constexpr int FIT = (227 * 1024 - FIXED_SMEM) / (STAGE_TX + 16);
   static constexpr int STAGES = STAGES_ ? STAGES_ : (FIT < 8 ? FIT : 8);
   static_assert(STAGES >= 2, "pipeline depth");
+  // LIFT: an X block, its partner and their C block are in the ring at once
+  static_assert(!LIFT || STAGES >= 3, "in-SM lifting needs >= 3 ring stages");
   static constexpr int OFF_A = 0;
   static constexpr int OFF_B = OFF_A + STAGES * A_STAGE;
   static constexpr int OFF_E = OFF_B + STAGES * B_STAGE;
   static constexpr int OFF_EPI = OFF_E + STAGES * E_STAGE;
   static constexpr int OFF_BAR = OFF_EPI + EPI_WARPS * EPI_WARP;
-  static constexpr int NUM_BARS = 2 * STAGES + 4;
+  static constexpr int NUM_BARS = 3 * STAGES + 4;  // full, empty, xfull (LIFT) per stage; tfull, tempty
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16 + 1024;  // + alignment slack
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
   static constexpr uint32_t C_FMT = KIND == MmaKind::I8 ? 2u : 1u;
@@ -134,7 +152,6 @@ struct Params {
   int direct_vec;     // direct stores: 0 scalar, 1 rows 16-byte aligned (v4), 2 rows 32-byte aligned (v8)
   int stok_vec;       // s_tok is 16-byte aligned (float4 loads)
   uint32_t debug;
-  uint32_t store_gap_ns;      // register-staged epilogue: pause between 32-byte store rounds
   unsigned long long* trace;  // perf probing: per-tile clock64 stamps of CTA 0 (env SLSP_GEMM_TRACE = device ptr)
   uint32_t hints;     // kHint* L2 policies
   int group;          // weight tiles per raster band
@@ -258,10 +275,15 @@ SLSP_DEVINL void epilogue_chunk(const Params& p, const CUtensorMap* tmOut, uint8
   constexpr int NW = C::OUT == SLSP_OUT_RAW_NM ? NC : NC / 2;  // 32-bit output words per lane
   const uint32_t lane = lane_id();
   const int64_t row = row0 + lane;
-  // per-token scales: one coalesced load, shuffled to every lane
-  float st_lane = 0.f;
-  if constexpr (C::OUT != SLSP_OUT_RAW_NM)
-    st_lane = (lane < NC && t0 + lane < p.m) ? __ldg(p.s_tok + t0 + lane) : 0.f;
+  // per-token scales: coalesced loads (32 tokens per load), shuffled to every lane
+  constexpr int NST = NC > 32 ? NC / 32 : 1;
+  float st_lane[NST];
+#pragma unroll
+  for (int j = 0; j < NST; ++j) {
+    st_lane[j] = 0.f;
+    if constexpr (C::OUT != SLSP_OUT_RAW_NM)
+      st_lane[j] = (32 * j + lane < NC && t0 + 32 * j + lane < p.m) ? __ldg(p.s_tok + t0 + 32 * j + lane) : 0.f;
+  }
   uint32_t w[NW];
   if constexpr (C::OUT == SLSP_OUT_RAW_NM) {
 #pragma unroll
@@ -269,8 +291,10 @@ SLSP_DEVINL void epilogue_chunk(const Params& p, const CUtensorMap* tmOut, uint8
   } else {
 #pragma unroll
     for (int i = 0; i < NW; ++i) {
-      const float lo = dequant<typename C::Acc>(r[2 * i], sc, __shfl_sync(0xffffffffu, st_lane, 2 * i));
-      const float hi = dequant<typename C::Acc>(r[2 * i + 1], sc, __shfl_sync(0xffffffffu, st_lane, 2 * i + 1));
+      const float s0 = __shfl_sync(0xffffffffu, st_lane[(2 * i) >> 5], (2 * i) & 31);
+      const float s1 = __shfl_sync(0xffffffffu, st_lane[(2 * i + 1) >> 5], (2 * i + 1) & 31);
+      const float lo = dequant<typename C::Acc>(r[2 * i], sc, s0);
+      const float hi = dequant<typename C::Acc>(r[2 * i + 1], sc, s1);
       w[i] = pack_bf16(lo, hi);
     }
   }
@@ -350,7 +374,8 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   uint8_t* sE = smem + C::OFF_E;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* empty = full + C::STAGES;
-  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* xfull = empty + C::STAGES;  // LIFT: this CTA's X tile of a stage has landed
+  uint64_t* tfull = xfull + C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -365,10 +390,19 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   const int m_super = (p.m_tiles + C::NPAIR - 1) / C::NPAIR;  // weight tiles per cluster step
   const int num_tiles = m_super * p.n_tiles;
 
+#ifdef SLSP_WATCHDOG
+  if (threadIdx.x == 0 && blockIdx.x < 2)
+    printf("SLSP layout block %d: smem %u A %u B %u E %u EPI %u full %u empty %u xfull %u tfull %u stages %d threads %d\n",
+           blockIdx.x, smem_u32(smem), smem_u32(sA), smem_u32(sB), smem_u32(sE), smem_u32(smem + C::OFF_EPI),
+           smem_u32(full), smem_u32(empty), smem_u32(xfull), smem_u32(tfull), C::STAGES, C::THREADS);
+#endif
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], C::NPAIR);  // every pair's MMA must be done with a stage (multicast B)
+      // LIFT: + one arrival per lift warp of both CTAs ("X present" / "C built")
+      mbar_init(&full[s], 1 + 2 * C::LIFT_WARPS);
+      // MMA commit (+ LIFT: each local lift warp is done reading the stage's X tile)
+      mbar_init(&empty[s], C::NPAIR + C::LIFT_WARPS);
+      mbar_init(&xfull[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -417,26 +451,42 @@ __global__ void __launch_bounds__(C::THREADS, 1)
           } else {
             mbar_wait(&empty[stage], phase ^ 1);
           }
+          // LIFT: k-blocks come in periods of 3 (X, X, C); C blocks load no activations
+          const bool xstage = !C::LIFT || kb % 3 != 2;
           if (no_load) {
             if (leader) mbar_arrive(&full[stage]);
+            if (C::LIFT) mbar_arrive(&xfull[stage]);
           } else {
             const bool skip_e = p.debug & kDbgNoMeta;
             if (p.trace && blockIdx.x == 0 && it < 16 && kb < 256) p.trace[65536 + (it * 256 + kb) * 2] = clock64();
-            if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (C::STAGE_TX - (skip_e ? C::E_STAGE : 0)));
+            const bool skip_b = !C::LIFT && (p.debug & kDbgSkipB3) && kb % 3 == 2;
+            if (leader)
+              mbar_arrive_expect_tx(&full[stage], 2 * (C::STAGE_TX - (skip_e ? C::E_STAGE : 0) -
+                                                       ((skip_b || C::LIFT) ? C::B_STAGE : 0)));
             const uint32_t bar = mapa_shared(smem_u32(&full[stage]), lead);
 #pragma unroll
             for (int h = 0; h < C::MSUB; ++h)
               tma_load_2d_cg2_hint(sA + stage * C::A_STAGE + h * C::A_SUB, &tmA, bar, kl * C::A_ROW, a_row + h * 256,
                                    pol_a);
+            if constexpr (C::LIFT) {
+              // X block j of period q: source bytes [512q + 256j, +256) into this CTA (local barrier)
+              // xfull completes once per ring lap (slots alternate between X
+              // and C blocks when STAGES % 3 != 0): C blocks arrive without bytes
+              if (!xstage) mbar_arrive(&xfull[stage]);
+              if (xstage) {
+                mbar_arrive_expect_tx(&xfull[stage], C::B_STAGE);
+                const int k0 = (kl / 3) * 512 + (kl % 3) * 256;
 #pragma unroll
-            for (int at = 0; at < C::B_ATOMS; ++at) {
-              uint8_t* dst = sB + stage * C::B_STAGE + at * C::B_ATOM;
-              if constexpr (C::NPAIR == 1) {
-                tma_load_2d_cg2_hint(dst, &tmB, bar, kl * C::K_BYTES_B + at * 128, b_row, pol_b);
-              } else {  // this pair fetches slice `pair` of the box for the same-rank CTA of every pair
-                const uint16_t mask = static_cast<uint16_t>((1u << rank) | (1u << (rank + 2)));
-                tma_load_2d_cg2_mc(dst + pair * C::B_PART * 128, &tmB, bar, kl * C::K_BYTES_B + at * 128,
-                                   b_row + static_cast<int>(pair) * C::B_PART, mask, pol_b);
+                for (int at = 0; at < C::B_ATOMS; ++at)
+                  tma_load_2d_hint(sB + stage * C::B_STAGE + at * C::B_ATOM, &tmB, smem_u32(&xfull[stage]),
+                                   k0 + at * 128, b_row, pol_b);
+              }
+            } else {
+#pragma unroll
+              for (int at = 0; at < C::B_ATOMS; ++at) {
+                if (skip_b) break;
+                tma_load_2d_cg2_hint(sB + stage * C::B_STAGE + at * C::B_ATOM, &tmB, bar, kl * C::K_BYTES_B + at * 128,
+                                     b_row, pol_b);
               }
             }
             if constexpr (C::SPARSE)  // one contiguous 4 KB tiled-metadata block per stage and subtile
@@ -444,9 +494,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
 #pragma unroll
                 for (int h = 0; h < C::MSUB; ++h)
                   tma_load_2d_cg2_hint(sE + stage * C::E_STAGE + h * C::E_SUB, &tmE, bar, 0,
-                                       C::KH ? (((a_row + h * 256) >> 7) * (p.num_kb >> 1) + (kl >> 1)) * 16 + (kl & 1) * 8
-                                             : (((a_row + h * 256) >> 7) * p.num_kb + kl) * 16,
-                                       pol_a);
+                                       (((a_row + h * 256) >> 7) * p.num_kb + kl) * 16, pol_a);
           }
           if (++stage == C::STAGES) {
             stage = 0;
@@ -481,8 +529,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
           if (no_mma) return;
           const uint32_t a_base = smem_u32(sA + st * C::A_STAGE + h * C::A_SUB);
           const uint32_t b_base = smem_u32(sB + st * C::B_STAGE);
-          // KH: alternate halves of the subtile's 8 metadata columns between stages
-          const uint32_t e_col = C::E_COL + 8 * h + (C::KH ? 4 * (kb & 1) : 0);
+          const uint32_t e_col = C::E_COL + 8 * h;
           if constexpr (C::SPARSE) {
             const uint32_t e_base = smem_u32(sE + st * C::E_STAGE + h * C::E_SUB);
 #pragma unroll
@@ -554,13 +601,84 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         tc_commit_mc(&tfull[acc], static_cast<uint16_t>(0x3u << lead));  // this pair's epilogues
       }
     }
+  } else if (C::LIFT && warp >= 2 + C::EPI_WARPS) {
+    // ------------------------------------------------ lift warps ----
+    // Follow the producer's stage sequence. X block (j = kb % 3 < 2): relay
+    // "X present" to the MMA issuer (leader's full barrier), then build C atom
+    // j of the period's C block from it: for each token row and 4-block chunk
+    // q, window 1 of blocks 4q..4q+3 = bytes 2-5 of each 8-byte block, read as
+    // two 16-byte X chunks, written as one 16-byte C chunk, both in the 128B
+    // swizzle the UMMA descriptor expects (chunk index ^= row & 7). C block:
+    // relay "C built" (after both atoms). Each warp owns B_ROWS / LIFT_WARPS
+    // rows; a quarter-warp touches 8 consecutive rows of one chunk column, so
+    // every 16-byte access is bank-conflict free.
+    if constexpr (C::LIFT) {
+      const uint32_t lw = warp - 2 - C::EPI_WARPS;
+      const uint32_t lane = lane_id();
+      const uint32_t full_lead = mapa_shared(smem_u32(&full[0]), lead);
+      constexpr int ROWS = C::B_ROWS / C::LIFT_WARPS;
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          const int j = kb % 3;
+          if (j < 2) {
+            mbar_wait(&xfull[stage], phase);
+            __syncwarp();
+            // (plain arrive: the relay publishes no data of its own; a
+            // .release.cluster arrive costs a MEMBAR.GPU per stage)
+            if (lane == 0) mbar_arrive_cluster(full_lead + 8u * stage);  // this CTA's X tile present
+            int cs = stage + 2 - j;  // ring slot of this period's C block
+            uint32_t cph = phase;
+            if (cs >= C::STAGES) {
+              cs -= C::STAGES;
+              cph ^= 1u;
+            }
+            if (j == 0) mbar_wait(&empty[cs], cph ^ 1u);  // C slot's previous occupant consumed
+            const uint32_t src = smem_u32(sB + stage * C::B_STAGE);
+            const uint32_t dst = smem_u32(sB + cs * C::B_STAGE + j * C::B_ATOM);
+#pragma unroll
+            for (int i = 0; i < ROWS / 8 * 2; ++i) {
+              if (p.debug & kDbgNoBuild) break;
+              const uint32_t r = lw * ROWS + (i >> 1) * 8 + (lane & 7);
+              const uint32_t q = (i & 1) * 4 + (lane >> 3);  // C chunk: blocks 4q..4q+3 of the X tile
+              const uint32_t sw = r & 7;
+              const uint32_t xa = src + (q >> 2) * C::B_ATOM + r * 128;  // X chunks 2q, 2q+1 live in atom q / 4
+              const uint4 x0 = ld_shared_u4(xa + (((2 * q) & 7) ^ sw) * 16);
+              const uint4 x1 = ld_shared_u4(xa + (((2 * q + 1) & 7) ^ sw) * 16);
+              st_shared_v4(dst + r * 128 + ((q ^ sw) << 4), __byte_perm(x0.x, x0.y, 0x5432),
+                           __byte_perm(x0.z, x0.w, 0x5432), __byte_perm(x1.x, x1.y, 0x5432),
+                           __byte_perm(x1.z, x1.w, 0x5432));
+            }
+            if (!(p.debug & kDbgNoFence)) fence_async_smem();  // generic-proxy writes -> visible to the tensor core
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);  // done reading this X tile
+          } else {
+            mbar_wait(&xfull[stage], phase);  // keeps this slot's xfull phase in step (no bytes for C blocks)
+            __syncwarp();
+            if (lane == 0) {
+              // the C writes were fenced to the async proxy after each atom
+              mbar_arrive_cluster(full_lead + 8u * stage);  // C block built (both atoms)
+              mbar_arrive(&empty[stage]);
+            }
+          }
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
   } else if constexpr (C::REG_EPI) {
     // ------------------------------------ register-staged epilogue ----
-    // 8 warps: two per TMEM lane quarter, each owning half of the tile's
-    // columns. Per subtile: tcgen05.ld (software-pipelined, 16 columns at a
-    // time) -> dequant -> BF16 pairs in registers -> release the subtile's
-    // TMEM to the MMA warp. Stores (32 B per lane) come after both releases
-    // when the two subtiles fit in registers (BN <= 224), else per subtile.
+    // 8 warps: two per TMEM lane quarter; the first owns columns [0, H0) of
+    // the tile, the second [H0, BN) (H0 = BN/2 rounded up to a 32-column
+    // box). Per subtile: tcgen05.ld (software-pipelined, 16 columns at a time)
+    // -> dequant -> BF16 pairs in registers -> release the subtile's TMEM to
+    // the MMA warp. Both subtiles are drained before any store, so the MMA
+    // waits only for the TMEM reads. Stores: 32-row x 32-column TMA boxes
+    // through a warp-private 2 KB staging buffer (64-byte swizzled rows) —
+    // per-lane 32-byte global stores cost measurably more L2 throughput.
     // Scales are fetched before the accumulator wait: s_ch into registers,
     // the warp's s_tok slice into a warp-private smem slice (LDS.128 broadcast).
     const uint32_t quarter = warp & 3;
@@ -568,78 +686,99 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     const uint32_t lane = lane_id();
     const uint64_t pol = (p.hints & kHintOutFirst) ? policy_evict_first() : policy_evict_normal();
     float* stok_sm = reinterpret_cast<float*>(smem + C::OFF_EPI + (warp - 2) * C::EPI_WARP);
-    constexpr int HALF = C::BN / 2;
-    constexpr bool HOLD_BOTH = C::REG_CHUNKS <= 7;
+    uint8_t* stage = smem + C::OFF_EPI + (warp - 2) * C::EPI_WARP + C::H0 * 4;
+    constexpr int NCH = C::H0 / 16;
+    const int ncols = half ? C::BN - C::H0 : C::H0;  // warp-uniform
+    const int nch = ncols / 16;
     int it = 0;
     for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
       int ms, nt;
       tile_coords(tile, p, m_super, ms, nt);
       const int mt = ms * C::NPAIR + static_cast<int>(pair);
-      const int64_t tcol0 = static_cast<int64_t>(nt) * C::BN + half * HALF;
-      const int64_t row0 = static_cast<int64_t>(mt) * C::BM + rank * C::A_ROWS + quarter * 32 + lane;
+      const int64_t tcol0 = static_cast<int64_t>(nt) * C::BN + half * C::H0;
+      const int64_t rowq = static_cast<int64_t>(mt) * C::BM + rank * C::A_ROWS + quarter * 32;  // lane 0's row
+      const int64_t row0 = rowq + lane;
       const float sc0 = row0 < p.n ? __ldg(p.s_ch + row0) : 0.f;
       const float sc1 = row0 + 256 < p.n ? __ldg(p.s_ch + row0 + 256) : 0.f;
-#pragma unroll
-      for (int i = static_cast<int>(lane); i < HALF; i += 32)
+      for (int i = static_cast<int>(lane); i < ncols; i += 32)
         stok_sm[i] = tcol0 + i < p.m ? __ldg(p.s_tok + tcol0 + i) : 0.f;
       __syncwarp();
       mbar_wait(&tfull[0], it & 1);
       tc_fence_after();
       if (warp == 2 && lane == 0) SLSP_TRACE(it, 3);
 
-      auto drain = [&](int h, float sc, uint32_t (&pk)[C::REG_CHUNKS][8]) {
-        const uint32_t t_base = tmem + ((quarter * 32) << 16) + h * C::ACC_COLS + half * HALF;
+      auto drain = [&](int h, float sc, uint32_t (&pk)[NCH][8]) {
+        const uint32_t t_base = tmem + ((quarter * 32) << 16) + h * C::ACC_COLS + half * C::H0;
         uint32_t r[2][16];
         tmem_ld_32x32b_x16(t_base, r[0]);
         tmem_ld_wait_regs(r[0]);
 #pragma unroll
-        for (int c = 0; c < C::REG_CHUNKS; ++c) {
-          if (c + 1 < C::REG_CHUNKS) tmem_ld_32x32b_x16(t_base + (c + 1) * 16, r[(c + 1) & 1]);
-          dequant16_smem<typename C::Acc>(r[c & 1], sc, smem_u32(stok_sm) + c * 64, pk[c]);
-          reg_pin(pk[c]);  // keep the math before the TMEM release (no sinking into the stores)
-          if (c + 1 < C::REG_CHUNKS) tmem_ld_wait_regs(r[(c + 1) & 1]);
+        for (int c = 0; c < NCH; ++c) {
+          if (c < nch) {
+            if (c + 1 < nch) tmem_ld_32x32b_x16(t_base + (c + 1) * 16, r[(c + 1) & 1]);
+            dequant16_smem<typename C::Acc>(r[c & 1], sc, smem_u32(stok_sm) + c * 64, pk[c]);
+            reg_pin(pk[c]);  // keep the math before the TMEM release (no sinking into the stores)
+            if (c + 1 < nch) tmem_ld_wait_regs(r[(c + 1) & 1]);
+          }
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[h]), lead));
         if (warp == 2 && lane == 0) SLSP_TRACE(it, 4 + 2 * h);
       };
-      auto store = [&](int h, const uint32_t (&pk)[C::REG_CHUNKS][8]) {
-        const int64_t row = row0 + h * 256;
-        if ((p.debug & kDbgNoStore) || row >= p.n) return;
-        uint8_t* dst_row = reinterpret_cast<uint8_t*>(p.out) + (row * p.ldo + tcol0) * 2;
-        if (p.direct_vec == 2 && tcol0 + HALF <= p.m) {
+      auto store = [&](int h, const uint32_t (&pk)[NCH][8]) {
+        if (p.debug & kDbgNoStore) return;
+        const int64_t rq = rowq + h * 256;
+        if (rq >= p.n) return;  // warp-uniform
+        if (p.tma_store) {
+          const uint32_t sb = smem_u32(stage);
 #pragma unroll
-          for (int c = 0; c < C::REG_CHUNKS; ++c) {
-            st_global_v8_hint(dst_row + c * 32, pk[c], pol);
-            if (p.store_gap_ns) __nanosleep(p.store_gap_ns);  // pace the output stream under the next mainloop
+          for (int b = 0; b < NCH / 2; ++b) {
+            const int64_t t0 = tcol0 + 32 * b;
+            if (2 * b >= nch || t0 >= p.m) break;  // warp-uniform
+            if (lane == 0) bulk_wait_read<0>();  // staging buffer read by the previous box's store
+            __syncwarp();
+            // [32 rows][64 B] staging in the map's 64-byte swizzle (16-byte chunk ^= (row >> 1) & 3)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const uint32_t(&w)[8] = pk[2 * b + (j >> 1)];
+              const int o = 4 * (j & 1);
+              st_shared_v4(sb + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4), w[o], w[o + 1], w[o + 2], w[o + 3]);
+            }
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d_hint(&tmOut, stage, static_cast<int>(t0), static_cast<int>(rq), pol);
+              bulk_commit();
+            }
           }
-        } else {  // token tail or unaligned rows: element stores from a local copy (cold path)
-          uint32_t tmp[C::REG_CHUNKS * 8];
+          return;
+        }
+        const int64_t row = row0 + h * 256;
+        if (row >= p.n) return;
+        uint8_t* dst_row = reinterpret_cast<uint8_t*>(p.out) + (row * p.ldo + tcol0) * 2;
+        if (p.direct_vec == 2 && tcol0 + ncols <= p.m) {
 #pragma unroll
-          for (int c = 0; c < C::REG_CHUNKS; ++c)
+          for (int c = 0; c < NCH; ++c)
+            if (c < nch) st_global_v8_hint(dst_row + c * 32, pk[c], pol);
+        } else {  // token tail or unaligned rows: element stores from a local copy (cold path)
+          uint32_t tmp[NCH * 8];
+#pragma unroll
+          for (int c = 0; c < NCH; ++c)
 #pragma unroll
             for (int i = 0; i < 8; ++i) tmp[c * 8 + i] = pk[c][i];
-          store_tail_u16(reinterpret_cast<uint16_t*>(dst_row), tmp, static_cast<int>(imin64(HALF, p.m - tcol0)));
+          store_tail_u16(reinterpret_cast<uint16_t*>(dst_row), tmp, static_cast<int>(imin64(ncols, p.m - tcol0)));
         }
       };
-      if constexpr (HOLD_BOTH) {
-        uint32_t pk0[C::REG_CHUNKS][8], pk1[C::REG_CHUNKS][8];
-        drain(0, sc0, pk0);
-        drain(1, sc1, pk1);
-        store(0, pk0);
-        if (warp == 2 && lane == 0) SLSP_TRACE(it, 5);
-        store(1, pk1);
-      } else {
-        uint32_t pk[C::REG_CHUNKS][8];
-        drain(0, sc0, pk);
-        store(0, pk);
-        if (warp == 2 && lane == 0) SLSP_TRACE(it, 5);
-        drain(1, sc1, pk);
-        store(1, pk);
-      }
+      uint32_t pk0[NCH][8], pk1[NCH][8];
+      drain(0, sc0, pk0);
+      drain(1, sc1, pk1);
+      store(0, pk0);
+      if (warp == 2 && lane == 0) SLSP_TRACE(it, 5);
+      store(1, pk1);
       if (warp == 2 && lane == 0) SLSP_TRACE(it, 7);
     }
+    if (lane == 0) bulk_wait<0>();
   } else {
     // ------------------------------------------------ epilogue ----
     const uint32_t quarter = warp & 3;  // TMEM lane quarter this warp may access
@@ -711,12 +850,9 @@ EncodeTiledFn get_encode() {
   return fn;
 }
 
-uint32_t debug_flags() {
-  static uint32_t flags = [] {
-    const char* e = std::getenv("SLSP_GEMM_DEBUG");
-    return e ? static_cast<uint32_t>(std::strtoul(e, nullptr, 0)) : 0u;
-  }();
-  return flags;
+uint32_t debug_flags() {  // read per call so one probe process can sweep it
+  const char* e = std::getenv("SLSP_GEMM_DEBUG");
+  return e ? static_cast<uint32_t>(std::strtoul(e, nullptr, 0)) : 0u;
 }
 
 // Tuning knob from the environment (read per call: cheap, and lets probes vary it).
@@ -803,10 +939,10 @@ void select_epilogue(Params& p, int out_mode, uint32_t msub, const void* out, in
   const int64_t row_bytes = ldo * esz;
   p.direct_vec = (base % 32 == 0 && row_bytes % 32 == 0) ? 2 : (base % 16 == 0 && row_bytes % 16 == 0) ? 1 : 0;
   p.stok_vec = (reinterpret_cast<uintptr_t>(s_tok) % 16) == 0;
-  // MSUB=2 BF16 [N][M] uses the register-staged epilogue (direct stores);
-  // otherwise TMA staging where rows are 16-byte aligned, unless overridden
-  const bool aligned = p.tma_store != 0;  // make_map_out enables TMA iff rows are 16-byte aligned
-  if (out_mode != SLSP_OUT_BF16_MN && aligned && (epi == 2 || (epi == 0 && msub == 2))) p.tma_store = 0;
+  // TMA staging where rows are 16-byte aligned (make_map_out enables it),
+  // direct vector stores when SLSP_GEMM_EPI=2 (perf probing)
+  (void)msub;
+  if (out_mode != SLSP_OUT_BF16_MN && p.tma_store && epi == 2) p.tma_store = 0;
 }
 
 int num_sms() {
@@ -855,54 +991,39 @@ int run(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const 
   return SLSP_OK;
 }
 
-template <bool SPARSE, MmaKind K, int BN, int CL, int MSUB, int KH>
+template <bool SPARSE, MmaKind K, int BN, int MSUB, int LIFT, int EW>
 int run_out_cl(int out_mode, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const CUtensorMap& o,
                const Params& p, cudaStream_t s) {
   switch (out_mode) {  // STAGES = 0: as many as fit
-    case SLSP_OUT_RAW_NM: return run<Cfg<SPARSE, K, BN, 0, SLSP_OUT_RAW_NM, CL, MSUB, KH>>(a, b, e, o, p, s);
-    case SLSP_OUT_BF16_NM: return run<Cfg<SPARSE, K, BN, 0, SLSP_OUT_BF16_NM, CL, MSUB, KH>>(a, b, e, o, p, s);
-    case SLSP_OUT_BF16_MN: return run<Cfg<SPARSE, K, BN, 0, SLSP_OUT_BF16_MN, CL, MSUB, KH>>(a, b, e, o, p, s);
+    case SLSP_OUT_RAW_NM: return run<Cfg<SPARSE, K, BN, 0, SLSP_OUT_RAW_NM, MSUB, LIFT, EW>>(a, b, e, o, p, s);
+    case SLSP_OUT_BF16_NM: return run<Cfg<SPARSE, K, BN, 0, SLSP_OUT_BF16_NM, MSUB, LIFT, EW>>(a, b, e, o, p, s);
+    case SLSP_OUT_BF16_MN: return run<Cfg<SPARSE, K, BN, 0, SLSP_OUT_BF16_MN, MSUB, LIFT, EW>>(a, b, e, o, p, s);
   }
   return SLSP_ERR_INVALID;
 }
 
-// Tile shape knobs: cluster 2 (one CTA pair) or 4 (two pairs sharing
-// activation tiles by TMA multicast), 1 or 2 M-subtiles per pair, and (sparse)
-// half k-stages; env SLSP_GEMM_CLUSTER / SLSP_GEMM_MSUB / SLSP_GEMM_KHALF
-// override the per-kernel defaults.
-template <bool SPARSE, MmaKind K, int BN, int KH>
-int run_out_kh(int out_mode, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const CUtensorMap& o,
-               const Params& p, cudaStream_t s, uint32_t cluster, uint32_t msub) {
-  if (cluster == 4)
-    return msub == 2 ? run_out_cl<SPARSE, K, BN, 4, 2, KH>(out_mode, a, b, e, o, p, s)
-                     : run_out_cl<SPARSE, K, BN, 4, 1, KH>(out_mode, a, b, e, o, p, s);
-  return msub == 2 ? run_out_cl<SPARSE, K, BN, 2, 2, KH>(out_mode, a, b, e, o, p, s)
-                   : run_out_cl<SPARSE, K, BN, 2, 1, KH>(out_mode, a, b, e, o, p, s);
-}
-
-template <bool SPARSE, MmaKind K, int BN>
+// Tile shape knobs: 1 or 2 M-subtiles per CTA pair (env SLSP_GEMM_MSUB for
+// the sparse kernel, SLSP_DGEMM_MSUB for the dense one); SLSP_GEMM_EPIW=32
+// forces 32-column epilogue chunks for one-subtile tiles (perf probing).
+template <bool SPARSE, MmaKind K, int BN, int LIFT = 0>
 int run_out(int out_mode, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const CUtensorMap& o,
-            const Params& p, cudaStream_t s, uint32_t cluster, uint32_t msub, uint32_t kh) {
-  if constexpr (SPARSE)
-    if (kh) return run_out_kh<SPARSE, K, BN, 1>(out_mode, a, b, e, o, p, s, cluster, msub);
-  return run_out_kh<SPARSE, K, BN, 0>(out_mode, a, b, e, o, p, s, cluster, msub);
+            const Params& p, cudaStream_t s, uint32_t msub, uint32_t ew) {
+  if (msub == 2) return run_out_cl<SPARSE, K, BN, 2, LIFT, 0>(out_mode, a, b, e, o, p, s);
+  if (!LIFT && ew == 32) return run_out_cl<SPARSE, K, BN, 1, 0, 32>(out_mode, a, b, e, o, p, s);
+  return run_out_cl<SPARSE, K, BN, 1, LIFT, 0>(out_mode, a, b, e, o, p, s);
 }
 
 constexpr int kSparseBN = 224;
 constexpr int kDenseBN = 256;
-constexpr uint32_t kSparseCluster = 2;
-constexpr uint32_t kDenseCluster = 2;
 constexpr uint32_t kDenseMsub = 1;
-constexpr uint32_t kSparseKHalf = 0;
-constexpr uint32_t kStoreGapNs = 0;
 constexpr uint32_t kRasterGroup = 16;  // measured best of {4, 8, 16, 32, 148} on Qwen2.5-7B shapes
 
 // M-subtiles for the sparse kernel: two subtiles (512 weight rows per pair,
 // activation tile shared) move 29% fewer operand bytes per MAC but halve the
 // tile count; use them unless that leaves a partial last wave the one-subtile
 // grid would not have (measured on Qwen2.5-7B shapes).
-uint32_t sparse_msub(int64_t n, int64_t m, uint32_t cluster) {
-  const int64_t clusters = num_sms() / static_cast<int64_t>(cluster);
+uint32_t sparse_msub(int64_t n, int64_t m) {
+  const int64_t clusters = num_sms() / 2;
   const int64_t nt = (m + kSparseBN - 1) / kSparseBN;
   const int64_t t1 = (n + 255) / 256 * nt, t2 = (n + 511) / 512 * nt;
   const int64_t w1 = (t1 + clusters - 1) / clusters, w2 = (t2 + clusters - 1) / clusters;
@@ -923,13 +1044,13 @@ int check_out(int out_mode, const float* s_ch, const float* s_tok, void* out, in
   return SLSP_OK;
 }
 
-}  // namespace
-
-extern "C" {
-
-int slsp_sparse_gemm(int dtype, const void* values, const uint8_t* meta, int64_t n, int64_t kp, const void* act,
-                     int64_t m, const float* s_ch, const float* s_tok, int out_mode, void* out, int64_t ldo,
-                     slsp_stream_t stream) {
+// Shared body of slsp_sparse_gemm (lifted activations, kp bytes per token)
+// and slsp_sparse_gemm_x (unlifted X, kx = 2kp/3 bytes per token, lifted in
+// shared memory; values/metadata in slsp_gemm_order's window order).
+template <bool LIFT>
+int sparse_entry(int dtype, const void* values, const uint8_t* meta, int64_t n, int64_t kp, const void* act,
+                 int64_t act_row, int64_t m, const float* s_ch, const float* s_tok, int out_mode, void* out,
+                 int64_t ldo, slsp_stream_t stream) {
   using namespace slsp_host;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (n < 0 || m < 0 || kp <= 0) return SLSP_ERR_INVALID;
@@ -943,31 +1064,47 @@ int slsp_sparse_gemm(int dtype, const void* values, const uint8_t* meta, int64_t
   if (n == 0 || m == 0) return SLSP_OK;
   CUtensorMap ta, tb, te, to;
   Params p{};
-  const uint32_t kh = env_knob("SLSP_GEMM_KHALF", kSparseKHalf) ? 1 : 0;
-  if ((st = make_map_2d(&ta, values, kp / 2, n, 128, kh ? 64 : 128))) return st;
-  // activation box: the CTA's half of the N tile, split once more across the
-  // pairs of a 4-CTA cluster (each pair fetches one slice and multicasts it)
-  const uint32_t cluster = env_knob("SLSP_GEMM_CLUSTER", kSparseCluster) == 4 ? 4 : 2;
-  const uint32_t msub = env_knob("SLSP_GEMM_MSUB", sparse_msub(n, m, cluster)) == 2 ? 2 : 1;
-  if ((st = make_map_2d(&tb, act, kp, m, kSparseBN / 2 / (cluster / 2)))) return st;
-  if ((st = make_map_meta(&te, meta, n, kp, kh ? 8 : 16))) return st;
-  if ((st = make_map_out(&to, out, out_mode, n, m, ldo, msub == 2 ? 16 : 32, &p.tma_store))) return st;
+  if ((st = make_map_2d(&ta, values, kp / 2, n, 128))) return st;
+  const uint32_t msub = env_knob("SLSP_GEMM_MSUB", sparse_msub(n, m)) == 2 ? 2 : 1;
+  const uint32_t ew = LIFT ? 0 : env_knob("SLSP_GEMM_EPIW", 0);
+  if ((st = make_map_2d(&tb, act, act_row, m, kSparseBN / 2))) return st;
+  if ((st = make_map_meta(&te, meta, n, kp))) return st;
+  if ((st = make_map_out(&to, out, out_mode, n, m, ldo, ew == 32 && msub == 1 ? 32 : epi_cols(msub, kSparseBN, out_mode),
+                         &p.tma_store)))
+    return st;
   select_epilogue(p, out_mode, msub, out, ldo, s_tok);
   p.n = n;
   p.m = m;
-  p.num_kb = static_cast<int>(kp / (kh ? 128 : 256));
+  p.num_kb = static_cast<int>(kp / 256);
   p.s_ch = s_ch;
   p.s_tok = s_tok;
   p.out = out;
   p.ldo = ldo;
   p.debug = debug_flags();
   p.trace = reinterpret_cast<unsigned long long*>(env_ptr("SLSP_GEMM_TRACE"));
-  p.store_gap_ns = env_knob("SLSP_GEMM_STORE_GAP", kStoreGapNs);
   p.hints = env_knob("SLSP_GEMM_HINTS", kDefaultHints);
   p.group = static_cast<int>(env_knob("SLSP_GEMM_GROUP", kRasterGroup));
-  if (dtype == SLSP_DT_I8)
-    return run_out<true, MmaKind::I8, kSparseBN>(out_mode, ta, tb, te, to, p, s, cluster, msub, kh);
-  return run_out<true, MmaKind::F8, kSparseBN>(out_mode, ta, tb, te, to, p, s, cluster, msub, kh);
+  constexpr int L = LIFT ? 1 : 0;
+  if (dtype == SLSP_DT_I8) return run_out<true, MmaKind::I8, kSparseBN, L>(out_mode, ta, tb, te, to, p, s, msub, ew);
+  return run_out<true, MmaKind::F8, kSparseBN, L>(out_mode, ta, tb, te, to, p, s, msub, ew);
+}
+
+}  // namespace
+
+extern "C" {
+
+int slsp_sparse_gemm(int dtype, const void* values, const uint8_t* meta, int64_t n, int64_t kp, const void* act,
+                     int64_t m, const float* s_ch, const float* s_tok, int out_mode, void* out, int64_t ldo,
+                     slsp_stream_t stream) {
+  return sparse_entry<false>(dtype, values, meta, n, kp, act, kp, m, s_ch, s_tok, out_mode, out, ldo, stream);
+}
+
+int slsp_sparse_gemm_x(int dtype, const void* values, const uint8_t* meta, int64_t n, int64_t kx, const void* act,
+                       int64_t m, const float* s_ch, const float* s_tok, int out_mode, void* out, int64_t ldo,
+                       slsp_stream_t stream) {
+  if (kx <= 0) return SLSP_ERR_INVALID;
+  if (kx % 512 != 0) return SLSP_ERR_DIMENSION;
+  return sparse_entry<true>(dtype, values, meta, n, kx / 2 * 3, act, kx, m, s_ch, s_tok, out_mode, out, ldo, stream);
 }
 
 int slsp_dense_gemm(int dtype, const void* w, int64_t n, int64_t k, const void* act, int64_t m, const float* s_ch,
@@ -987,10 +1124,10 @@ int slsp_dense_gemm(int dtype, const void* w, int64_t n, int64_t k, const void* 
   CUtensorMap ta, tb, to;
   Params p{};
   if ((st = make_map_2d(&ta, w, k * esz, n, 128))) return st;
-  const uint32_t cluster = env_knob("SLSP_GEMM_CLUSTER", kDenseCluster) == 4 ? 4 : 2;
-  const uint32_t msub = env_knob("SLSP_GEMM_MSUB", kDenseMsub) == 2 ? 2 : 1;
-  if ((st = make_map_2d(&tb, act, k * esz, m, kDenseBN / 2 / (cluster / 2)))) return st;
-  if ((st = make_map_out(&to, out, out_mode, n, m, ldo, msub == 2 ? 16 : 32, &p.tma_store))) return st;
+  const uint32_t msub = env_knob("SLSP_DGEMM_MSUB", kDenseMsub) == 2 ? 2 : 1;
+  const uint32_t ew = env_knob("SLSP_GEMM_EPIW", 0);
+  if ((st = make_map_2d(&tb, act, k * esz, m, kDenseBN / 2))) return st;
+  if ((st = make_map_out(&to, out, out_mode, n, m, ldo, ew == 32 && msub == 1 ? 32 : epi_cols(msub, kDenseBN, out_mode), &p.tma_store))) return st;
   select_epilogue(p, out_mode, msub, out, ldo, s_tok);
   p.n = n;
   p.m = m;
@@ -1001,14 +1138,13 @@ int slsp_dense_gemm(int dtype, const void* w, int64_t n, int64_t k, const void* 
   p.ldo = ldo;
   p.debug = debug_flags();
   p.trace = reinterpret_cast<unsigned long long*>(env_ptr("SLSP_GEMM_TRACE"));
-  p.store_gap_ns = env_knob("SLSP_GEMM_STORE_GAP", kStoreGapNs);
   p.hints = env_knob("SLSP_GEMM_HINTS", kDefaultHints);
   p.group = static_cast<int>(env_knob("SLSP_GEMM_GROUP", kRasterGroup));
   if (dtype == SLSP_DT_I8)
-    return run_out<false, MmaKind::I8, kDenseBN>(out_mode, ta, tb, ta, to, p, s, cluster, msub, 0);
+    return run_out<false, MmaKind::I8, kDenseBN>(out_mode, ta, tb, ta, to, p, s, msub, ew);
   if (dtype == SLSP_DT_E4M3)
-    return run_out<false, MmaKind::F8, kDenseBN>(out_mode, ta, tb, ta, to, p, s, cluster, msub, 0);
-  return run_out<false, MmaKind::F16, kDenseBN>(out_mode, ta, tb, ta, to, p, s, cluster, msub, 0);
+    return run_out<false, MmaKind::F8, kDenseBN>(out_mode, ta, tb, ta, to, p, s, msub, ew);
+  return run_out<false, MmaKind::F16, kDenseBN>(out_mode, ta, tb, ta, to, p, s, msub, ew);
 }
 
 }  // extern "C"

@@ -366,6 +366,50 @@ __global__ void tile_meta_kernel(const uint8_t* __restrict__ meta, int64_t rows,
   }
 }
 
+// slsp_gemm_order (6:8): output window i of a row, period P = i / 192,
+// o = i % 192: o < 128 -> block 64P + o/2, window 2*(o & 1); else block
+// 64P + o - 128, window 1. One thread per 16 output windows (2*ESZ value
+// bytes and one 4-bit code pair each). Offline, one pass over the weights.
+template <int ESZ>
+__global__ void gemm_order_kernel(const uint8_t* __restrict__ vals, const uint8_t* __restrict__ codes, int64_t rows,
+                                  int64_t nblk, int64_t kp_ref, uint8_t* __restrict__ vout, uint8_t* __restrict__ cout,
+                                  int64_t kp_out) {
+  const int64_t per_row = kp_out / 64;  // 16-window groups per output row
+  const int64_t total = rows * per_row;
+  const int64_t wref = kp_ref / 4;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t row = t / per_row;
+    const int64_t i0 = (t - row * per_row) * 16;
+    const uint8_t* vr = vals + row * (kp_ref / 2) * ESZ;
+    const uint8_t* cr = codes + row * (kp_ref / 8);
+    uint8_t v[32 * ESZ];
+    uint32_t c[2] = {0u, 0u};
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int64_t i = i0 + u;
+      const int64_t P = i / 192, o = i - P * 192;
+      const int64_t blk = o < 128 ? 64 * P + (o >> 1) : 64 * P + (o - 128);
+      const int64_t w = o < 128 ? 2 * (o & 1) : 1;
+      const int64_t j = blk * 3 + w;
+      uint32_t nib = 0x4u;  // padding window: values 0, codes (0,1)
+      if (blk < nblk && j < wref) {
+#pragma unroll
+        for (int b = 0; b < 2 * ESZ; ++b) v[u * 2 * ESZ + b] = vr[j * 2 * ESZ + b];
+        nib = (cr[j >> 1] >> (4 * (j & 1))) & 0xFu;
+      } else {
+#pragma unroll
+        for (int b = 0; b < 2 * ESZ; ++b) v[u * 2 * ESZ + b] = 0;
+      }
+      c[u >> 3] |= nib << (4 * (u & 7));
+    }
+    uint4* dv = reinterpret_cast<uint4*>(vout + (row * (kp_out / 2) + i0 * 2) * ESZ);
+#pragma unroll
+    for (int q = 0; q < 2 * ESZ; ++q) dv[q] = reinterpret_cast<const uint4*>(v)[q];
+    *reinterpret_cast<uint2*>(cout + row * (kp_out / 8) + i0 / 2) = make_uint2(c[0], c[1]);
+  }
+}
+
 template <int MODE>
 int launch_pack(int esz, PackArgs& a, cudaStream_t s) {
   const int64_t chunks = (a.group_slots + kThreads - 1) / kThreads;
@@ -495,6 +539,30 @@ int slsp_pack_compress(int dtype, const void* w, int64_t rows, int64_t cols, int
   a.status = status;
   if ((st = launch_pack<1>(esz, a, s))) return st;
   return status_collect(status_ws, s, SLSP_ERR_NOT_COMPLIANT, err_row, err_block);
+}
+
+int slsp_gemm_order(int dtype, const void* values, const uint8_t* codes, int64_t rows, int64_t cols, int64_t kp_ref,
+                    void* values_out, uint8_t* codes_out, int64_t kp_out, slsp_stream_t stream) {
+  using namespace slsp_host;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int esz = elem_size(dtype);
+  if ((esz != 1 && esz != 2) || rows < 0 || cols <= 0 || kp_ref <= 0 || kp_ref % 4 != 0) return SLSP_ERR_INVALID;
+  if (!values || !codes || !values_out || !codes_out) return SLSP_ERR_INVALID;
+  const int64_t nblk = (cols + 7) / 8;
+  if (kp_ref < nblk * 12) return SLSP_ERR_DIMENSION;  // the reference width must hold every real window
+  if (kp_out != (cols + 511) / 512 * 768) return SLSP_ERR_DIMENSION;
+  if ((reinterpret_cast<uintptr_t>(values_out) & 15u) || (reinterpret_cast<uintptr_t>(codes_out) & 7u))
+    return SLSP_ERR_INVALID;
+  int st;
+  if ((st = require_sm100())) return st;
+  const int64_t total = rows * (kp_out / 64);
+  if (total == 0) return SLSP_OK;
+  const auto* v = static_cast<const uint8_t*>(values);
+  auto* vo = static_cast<uint8_t*>(values_out);
+  if (esz == 1) gemm_order_kernel<1><<<grid_for(total, 256), 256, 0, s>>>(v, codes, rows, nblk, kp_ref, vo, codes_out, kp_out);
+  else gemm_order_kernel<2><<<grid_for(total, 256), 256, 0, s>>>(v, codes, rows, nblk, kp_ref, vo, codes_out, kp_out);
+  SLSP_LAUNCH_CHECK();
+  return SLSP_OK;
 }
 
 int64_t slsp_tiled_meta_bytes(int64_t rows, int64_t kp) { return (rows + 127) / 128 * 128 * (kp / 8); }

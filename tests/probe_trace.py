@@ -24,7 +24,14 @@ g = torch.Generator(device=dev).manual_seed(0)
 s_ch = torch.rand(N, device=dev, generator=g) + 0.5
 s_tok = torch.rand(M, device=dev, generator=g) + 0.5
 out = torch.empty((N, M), dtype=torch.bfloat16, device=dev)
-if kind == "sparse":
+if kind == "sparsex":
+    w = torch.randint(-127, 128, (N, K), dtype=torch.int8, device=dev, generator=g)
+    w = slsp.magnitude_prune(w, 6, 8)
+    pw = slsp.pack_compress(w, 6, 8)
+    go = pw.gemm_order()
+    act = torch.randint(-127, 128, (M, K), dtype=torch.int8, device=dev, generator=g)
+    run = lambda: slsp.sparse_gemm_x(go, act, s_ch, s_tok, slsp.OUT_BF16_NM, out=out)  # noqa: E731
+elif kind == "sparse":
     vals = torch.randint(-127, 128, (N, KP // 2), dtype=torch.int8, device=dev, generator=g)
     meta = torch.full((N, KP // 8), 0x44, dtype=torch.uint8, device=dev)
     pw = slsp.PackedWeights(vals, meta, N, K, KP, 6, 8)
