@@ -416,6 +416,26 @@ SLSP_DEVINL float2 fmul2_rn(float2 a, float2 b) {
   return d;
 }
 
+SLSP_DEVINL float2 fadd2_rn(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 a2, b2, d2;\n\t"
+      "mov.b64 a2, {%2, %3};\n\tmov.b64 b2, {%4, %5};\n\t"
+      "add.rn.f32x2 d2, a2, b2;\n\tmov.b64 {%0, %1}, d2;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+
+SLSP_DEVINL float2 fsub2_rn(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 a2, b2, d2;\n\t"
+      "mov.b64 a2, {%2, %3};\n\tmov.b64 b2, {%4, %5};\n\t"
+      "sub.rn.f32x2 d2, a2, b2;\n\tmov.b64 {%0, %1}, d2;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+
 // 32-byte global store (sm_100 STG.256) with an L2 cache-policy hint.
 SLSP_DEVINL void st_global_v8_hint(void* p, const uint32_t (&w)[8], uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8}, %9;" ::"l"(p), "r"(w[0]),
