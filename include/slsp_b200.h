@@ -120,6 +120,12 @@ SLSP_API int slsp_pack_compress(int dtype, const void* w, int64_t rows, int64_t 
  * holds ceil(rows/128)*128 * kp/8 bytes. kp % 256 == 0. */
 SLSP_API int slsp_tile_meta(const uint8_t* meta, int64_t rows, int64_t kp, uint8_t* tiled, slsp_stream_t stream);
 
+/* slsp_tile_meta for the operand type `dtype` of the sparse GEMM: I8/E4M3
+ * use the row-major atom above; BF16 (kind::f16) uses the 16-bit atom, the
+ * same bytes with byte-offset bits 1 and 7 of each 2 KB atom exchanged. */
+SLSP_API int slsp_tile_meta_ex(const uint8_t* meta, int64_t rows, int64_t kp, int dtype, uint8_t* tiled,
+                      slsp_stream_t stream);
+
 /* Bytes of the tiled metadata buffer for `rows` x `kp`. */
 SLSP_API int64_t slsp_tiled_meta_bytes(int64_t rows, int64_t kp);
 

@@ -103,6 +103,7 @@ def lib() -> C.CDLL:
                 "slsp_sparse_gemm": (i32, [i32, vp, vp, i64, i64, vp, i64, vp, vp, i32, vp, i64, vp]),
                 "slsp_dense_gemm": (i32, [i32, vp, i64, i64, vp, i64, vp, vp, i32, vp, i64, vp]),
                 "slsp_tile_meta": (i32, [vp, i64, i64, vp, vp]),
+                "slsp_tile_meta_ex": (i32, [vp, i64, i64, i32, vp, vp]),
                 "slsp_gemm_order": (i32, [i32, vp, vp, i64, i64, i64, vp, vp, i64, vp]),
                 "slsp_sparse_gemm_x": (i32, [i32, vp, vp, i64, i64, vp, i64, vp, vp, i32, vp, i64, vp]),
                 "slsp_tiled_meta_bytes": (i64, [i64, i64]),
@@ -229,7 +230,7 @@ class PackedWeights:
 
     def tiled(self) -> torch.Tensor:
         if self.meta_tiled is None:
-            self.meta_tiled = tile_meta(self.meta, self.n, self.kp)
+            self.meta_tiled = tile_meta(self.meta, self.n, self.kp, self.dtype)
         return self.meta_tiled
 
     def gemm_order(self) -> "GemmOrderWeights":
@@ -268,11 +269,11 @@ def gemm_order(w: PackedWeights) -> GemmOrderWeights:
     return GemmOrderWeights(values, tile_meta(codes, w.n, kp), w.n, w.k, kx, kp)
 
 
-def tile_meta(meta: torch.Tensor, rows: int, kp: int) -> torch.Tensor:
-    """Row-major codes -> the MMA-tiled metadata layout (slsp_tile_meta)."""
+def tile_meta(meta: torch.Tensor, rows: int, kp: int, dtype: int = DT_I8) -> torch.Tensor:
+    """Row-major codes -> the MMA-tiled metadata layout of operand type `dtype` (slsp_tile_meta_ex)."""
     _require_cuda(meta)
     out = torch.empty(int(lib().slsp_tiled_meta_bytes(rows, kp)), dtype=torch.uint8, device=meta.device)
-    _check(lib().slsp_tile_meta(_ptr(meta), rows, kp, _ptr(out), _stream(meta.device)), "tile_meta")
+    _check(lib().slsp_tile_meta_ex(_ptr(meta), rows, kp, dtype, _ptr(out), _stream(meta.device)), "tile_meta")
     return out
 
 

@@ -90,7 +90,12 @@ struct Cfg {
   static constexpr int B_ATOMS = SPARSE ? 2 : 1;             // B bytes per stage = 2x A bytes for .sp
   static constexpr int B_ATOM = B_ROWS * 128;
   static constexpr int B_STAGE = B_ATOM * B_ATOMS;
-  static constexpr int E_ATOMS = 2;                          // 128x128b metadata atoms per stage and subtile
+  // 128x128b metadata atoms per stage and subtile: a stage is 128 bytes of
+  // compressed A per row = 256 logical k for 8-bit kinds (2 atoms, 2 TMEM
+  // columns per K=64 MMA) and 128 logical k for BF16 (1 atom, 1 column per
+  // K=32 MMA); 1 metadata bit per logical k either way
+  static constexpr int E_ATOMS = KIND == MmaKind::F16 ? 1 : 2;
+  static constexpr int E_PER_MMA = KIND == MmaKind::F16 ? 1 : 2;
   static constexpr int E_SUB = SPARSE ? E_ATOMS * 128 * 16 : 0;
   static constexpr int E_STAGE = MSUB * E_SUB;
   static constexpr int STAGE_TX = A_STAGE + B_STAGE + E_STAGE;
@@ -494,7 +499,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
 #pragma unroll
                 for (int h = 0; h < C::MSUB; ++h)
                   tma_load_2d_cg2_hint(sE + stage * C::E_STAGE + h * C::E_SUB, &tmE, bar, 0,
-                                       (((a_row + h * 256) >> 7) * p.num_kb + kl) * 16, pol_a);
+                                       (((a_row + h * 256) >> 7) * p.num_kb + kl) * 8 * C::E_ATOMS, pol_a);
           }
           if (++stage == C::STAGES) {
             stage = 0;
@@ -543,7 +548,12 @@ __global__ void __launch_bounds__(C::THREADS, 1)
             const uint32_t d = d_tmem + h * C::ACC_COLS;
             if constexpr (C::SPARSE) {
               const uint64_t bdesc = smem_desc(b_base + (j >> 1) * C::B_ATOM + (j & 1) * 64, 16, 1024, 2);
-              umma_sparse_cg2<C::KIND>(d, adesc, bdesc, tmem + e_col + 2 * j, C::IDESC, acc_flag);
+              // 16-bit kinds: metadata column j is addressed as the even column
+              // j & ~1 plus the instruction descriptor's sparse_id2 = j & 1
+              // (bits 0-1); 8-bit kinds use two columns per MMA, id2 = 0
+              const uint32_t ecol = C::E_PER_MMA == 1 ? (j & ~1) : 2 * j;
+              const uint32_t idesc = C::E_PER_MMA == 1 ? (C::IDESC | static_cast<uint32_t>(j & 1)) : C::IDESC;
+              umma_sparse_cg2<C::KIND>(d, adesc, bdesc, tmem + e_col + ecol, idesc, acc_flag);
             } else {
               const uint64_t bdesc = smem_desc(b_base + j * 32, 16, 1024, 2);
               umma_dense_cg2<C::KIND>(d, adesc, bdesc, C::IDESC, acc_flag);
@@ -1059,23 +1069,25 @@ int sparse_entry(int dtype, const void* values, const uint8_t* meta, int64_t n, 
   if (n > (int64_t{1} << 31) - 256 || m > (int64_t{1} << 31) - 256) return SLSP_ERR_UNSUPPORTED;
   int st = check_out(out_mode, s_ch, s_tok, out, ldo, n, m);
   if (st) return st;
-  if (dtype != SLSP_DT_I8 && dtype != SLSP_DT_E4M3) return SLSP_ERR_UNSUPPORTED;
+  if (dtype != SLSP_DT_I8 && dtype != SLSP_DT_E4M3 && !(dtype == SLSP_DT_BF16 && !LIFT)) return SLSP_ERR_UNSUPPORTED;
   if ((st = require_sm100())) return st;
   if (n == 0 || m == 0) return SLSP_OK;
+  const int esz = dtype == SLSP_DT_BF16 ? 2 : 1;
   CUtensorMap ta, tb, te, to;
   Params p{};
-  if ((st = make_map_2d(&ta, values, kp / 2, n, 128))) return st;
+  if ((st = make_map_2d(&ta, values, kp / 2 * esz, n, 128))) return st;
   const uint32_t msub = env_knob("SLSP_GEMM_MSUB", sparse_msub(n, m)) == 2 ? 2 : 1;
   const uint32_t ew = LIFT ? 0 : env_knob("SLSP_GEMM_EPIW", 0);
-  if ((st = make_map_2d(&tb, act, act_row, m, kSparseBN / 2))) return st;
-  if ((st = make_map_meta(&te, meta, n, kp))) return st;
+  if ((st = make_map_2d(&tb, act, act_row * esz, m, kSparseBN / 2))) return st;
+  // BF16: a 128-byte A stage is 128 logical k -> one 2 KB metadata atom per stage
+  if ((st = make_map_meta(&te, meta, n, kp, esz == 2 ? 8 : 16))) return st;
   if ((st = make_map_out(&to, out, out_mode, n, m, ldo, ew == 32 && msub == 1 ? 32 : epi_cols(msub, kSparseBN, out_mode),
                          &p.tma_store)))
     return st;
   select_epilogue(p, out_mode, msub, out, ldo, s_tok);
   p.n = n;
   p.m = m;
-  p.num_kb = static_cast<int>(kp / 256);
+  p.num_kb = static_cast<int>(kp * esz / 256);
   p.s_ch = s_ch;
   p.s_tok = s_tok;
   p.out = out;
@@ -1086,6 +1098,8 @@ int sparse_entry(int dtype, const void* values, const uint8_t* meta, int64_t n, 
   p.group = static_cast<int>(env_knob("SLSP_GEMM_GROUP", kRasterGroup));
   constexpr int L = LIFT ? 1 : 0;
   if (dtype == SLSP_DT_I8) return run_out<true, MmaKind::I8, kSparseBN, L>(out_mode, ta, tb, te, to, p, s, msub, ew);
+  if constexpr (!LIFT)
+    if (dtype == SLSP_DT_BF16) return run_out<true, MmaKind::F16, kSparseBN>(out_mode, ta, tb, te, to, p, s, msub, ew);
   return run_out<true, MmaKind::F8, kSparseBN, L>(out_mode, ta, tb, te, to, p, s, msub, ew);
 }
 

@@ -41,9 +41,9 @@ struct ActArgs {
 };
 
 // Launch-path selection (env SLSP_LIFT_ROW, perf probing): 0 = warp path,
-// 1 (default) = one CTA per row (quads in registers), 2 = persistent CTAs
-// with a register double buffer, 3 = coalesced vector path (BF16 input, 6:8
-// lift / quantize_rows).
+// else (default) the row-resident path where it applies. (Measured and
+// dropped: persistent CTAs with a register double buffer, and a coalesced
+// one-block-per-lane layout — both slower on the Qwen/Llama K values.)
 int env_row_path() {
   const char* e = std::getenv("SLSP_LIFT_ROW");
   return e && *e ? e[0] - '0' : 1;
@@ -490,8 +490,6 @@ SLSP_DEVINL void row_emit(const ActArgs& a, int64_t row, int nquads, float* s_ma
   for (int i = nquads * G::OUT_VEC + tid; i < out_vecs; i += nthr) dst[i] = make_uint4(0, 0, 0, 0);  // kp padding
 }
 
-// Grid-stride over rows with a register double buffer: the next row's loads
-// are in flight while this row is reduced, quantized and stored.
 template <int IN, int KIND, int L, int QPT>
 __global__ void __launch_bounds__(1024) act_row1_kernel(ActArgs a) {  // one row per CTA, grid = rows
   using G = WarpGeom<IN, KIND, L>;
@@ -503,180 +501,9 @@ __global__ void __launch_bounds__(1024) act_row1_kernel(ActArgs a) {  // one row
 }
 
 template <int IN, int KIND, int L, int QPT>
-__global__ void __launch_bounds__(1024) act_row_kernel(ActArgs a) {
-  using G = WarpGeom<IN, KIND, L>;
-  __shared__ float s_max[32];
-  const int nquads = static_cast<int>(a.cols / G::ELEMS);
-  const int64_t stride = gridDim.x;
-  uint4 va[QPT][G::IN_VEC], vb[QPT][G::IN_VEC];
-  int64_t row = blockIdx.x;
-  row_load<IN, KIND, L, QPT>(a, row, nquads, va);
-  while (row < a.rows) {
-    row_load<IN, KIND, L, QPT>(a, row + stride, nquads, vb);
-    row_emit<IN, KIND, L, QPT>(a, row, nquads, s_max, va);
-    row += stride;
-    if (row >= a.rows) break;
-    row_load<IN, KIND, L, QPT>(a, row + stride, nquads, va);
-    row_emit<IN, KIND, L, QPT>(a, row, nquads, s_max, vb);
-    row += stride;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Coalesced vector path (the default for BF16 input; MODE 1 = 6:8 lift,
-// MODE 0 = quantize_rows): a 16-byte input vector is 8 consecutive elements =
-// one 8-block, so thread t of the row's CTA owns blocks t, t+T, ... and every
-// load instruction of a warp reads 512 contiguous bytes; all V loads of a
-// thread are issued before the first use (V >= 4 keeps >= 64 KB in flight per
-// SM). Codes of a block: 2 words; lifted: 3 words (windows 0, 1, 2 = code
-// bytes 0-3, 2-5, 4-7). A warp's 32 blocks are staged in smem (32-bit stores
-// at a 12-byte stride: conflict-free) and written as 16-byte vectors — 384
-// (lift) / 256 (quantize) contiguous bytes per warp.
-template <int KIND, int MODE, int V>
-__global__ void __launch_bounds__(512) act_vec_kernel(ActArgs a) {
-  constexpr int OW = MODE ? 3 : 2;  // output words per block
-  __shared__ float s_max[16];
-  __shared__ __align__(16) uint32_t stage[16][32 * OW];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int T = blockDim.x;
-  const int nblk = static_cast<int>(a.cols / 8);
-  const int64_t row = blockIdx.x;
-  const uint4* src = reinterpret_cast<const uint4*>(a.x + row * a.cols * 2);
-  uint4 v[V];
-#pragma unroll
-  for (int j = 0; j < V; ++j) {
-    const int b = tid + j * T;
-    v[j] = b < nblk ? __ldg(src + b) : make_uint4(0, 0, 0, 0);
-  }
-  // |x|max: packed bf16x2; NaN propagates and Inf wins (zero fill is neutral)
-  __nv_bfloat162 m2 = __float2bfloat162_rn(0.f);
-#pragma unroll
-  for (int j = 0; j < V; ++j) {
-    const uint32_t w[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
-#pragma unroll
-    for (int e = 0; e < 4; ++e) m2 = __hmax2_nan(m2, __habs2(*reinterpret_cast<const __nv_bfloat162*>(&w[e])));
-  }
-  float amax;
-  {
-    const float lo = __low2float(m2), hi = __high2float(m2);
-    amax = (isnan(lo) || isnan(hi)) ? __int_as_float(0x7fc00000) : fmaxf(lo, hi);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const float t = __shfl_xor_sync(0xffffffffu, amax, o);
-    amax = (isnan(t) || t > amax) ? t : amax;
-  }
-  if (lane == 0) s_max[warp] = amax;
-  __syncthreads();
-  amax = s_max[0];
-  for (int w = 1; w < (T >> 5); ++w) {
-    const float t = s_max[w];
-    amax = (isnan(t) || t > amax) ? t : amax;
-  }
-  if (!isfinite(amax) && tid == 0 && a.status) atomicMin(a.status, static_cast<unsigned long long>(row) << 32);
-  // quantize.hpp:151-153, in double
-  const double qmax = KIND == K_INT8 ? 127.0 : 448.0;
-  const double absmax = static_cast<double>(amax);
-  const double r = absmax == 0.0 ? 0.0 : qmax / absmax;
-  const float r32 = __double2float_rn(r);
-  if (tid == 0) a.scales[row] = absmax == 0.0 ? 1.0f : __double2float_rn(absmax / qmax);
-
-  uint8_t* dst = a.out + row * a.out_bytes;
-  uint32_t* st = stage[warp];
-#pragma unroll
-  for (int j = 0; j < V; ++j) {
-    const int b0 = j * T + warp * 32;  // first block of this warp's segment (warp-uniform)
-    if (b0 >= nblk) break;
-    const uint32_t w[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
-    uint32_t qw[2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      if constexpr (KIND == K_INT8) {
-        qw[h] = quant4_bf16_int8(w[2 * h], w[2 * h + 1], r32, r);
-        continue;
-      }
-      uint32_t c[4];
-#pragma unroll
-      for (int d = 0; d < 4; ++d) {
-        const uint32_t bits = (w[2 * h + (d >> 1)] >> (16 * (d & 1))) & 0xFFFFu;
-        const float x = __uint_as_float(bits << 16);
-        if constexpr (KIND == K_INT8) c[d] = quant_int8_fast(x, r32, r);
-        else c[d] = quant_code<KIND>(x, r);
-      }
-      qw[h] = __byte_perm(__byte_perm(c[0], c[1], 0x0040), __byte_perm(c[2], c[3], 0x0040), 0x5410);
-    }
-    if (b0 + lane >= nblk) qw[0] = qw[1] = 0u;  // zero padding windows
-    if constexpr (MODE) {
-      st[3 * lane] = qw[0];
-      st[3 * lane + 1] = __byte_perm(qw[0], qw[1], 0x5432);
-      st[3 * lane + 2] = qw[1];
-    } else {
-      st[2 * lane] = qw[0];
-      st[2 * lane + 1] = qw[1];
-    }
-    __syncwarp();
-    const int64_t off = static_cast<int64_t>(b0) * OW * 4 + lane * 16;
-    if (lane < OW * 8 && off < a.out_bytes) *reinterpret_cast<uint4*>(dst + off) = reinterpret_cast<const uint4*>(st)[lane];
-    __syncwarp();
-  }
-  // zero the row's padding past the last (32-block) warp segment
-  const int64_t done = static_cast<int64_t>((nblk + 31) / 32) * 32 * OW * 4;
-  for (int64_t i = done / 16 + tid; i < a.out_bytes / 16; i += T) reinterpret_cast<uint4*>(dst)[i] = make_uint4(0, 0, 0, 0);
-}
-
-template <int KIND, int MODE, int V>
-int launch_vec_v(ActArgs& a, int threads, cudaStream_t s) {
-  act_vec_kernel<KIND, MODE, V><<<static_cast<unsigned>(a.rows), threads, 0, s>>>(a);
-  SLSP_LAUNCH_CHECK();
-  return SLSP_OK;
-}
-
-// Coalesced vector path launch (BF16 input, whole 8-blocks, 16-byte aligned
-// rows); returns 0 when it does not apply.
-template <int KIND, int MODE>
-int launch_vec(ActArgs& a, cudaStream_t s, int* st) {
-  if (a.cols % 8 != 0 || a.out_bytes % 16 != 0 || a.rows >= (int64_t{1} << 31) || a.rows == 0) return 0;
-  if ((reinterpret_cast<uintptr_t>(a.x) | reinterpret_cast<uintptr_t>(a.out)) & 15u) return 0;
-  if (MODE && a.out_bytes < a.cols / 8 * 12) return 0;
-  const int64_t nblk = a.cols / 8;
-  static constexpr int Vs[] = {4, 6, 8, 12, 16};
-  int vv = 0;
-  for (int c : Vs)
-    if (nblk <= 512 * c) {
-      vv = c;
-      break;
-    }
-  if (!vv) return 0;
-  const int threads = static_cast<int>(((nblk + vv - 1) / vv + 31) / 32 * 32);
-  switch (vv) {
-    case 4: *st = launch_vec_v<KIND, MODE, 4>(a, threads, s); break;
-    case 6: *st = launch_vec_v<KIND, MODE, 6>(a, threads, s); break;
-    case 8: *st = launch_vec_v<KIND, MODE, 8>(a, threads, s); break;
-    case 12: *st = launch_vec_v<KIND, MODE, 12>(a, threads, s); break;
-    default: *st = launch_vec_v<KIND, MODE, 16>(a, threads, s); break;
-  }
-  return 1;
-}
-
-template <int IN, int KIND, int L, int QPT>
 int launch_row_q(ActArgs& a, int threads, cudaStream_t s) {
-  // persistent-ish grid: the resident CTAs of one wave, each streaming rows
-  static int cap[33] = {0};
-  const int slot = threads / 32;
-  if (!cap[slot]) {
-    int dev = 0, sms = 0, per_sm = 0;
-    SLSP_CUDA_TRY(cudaGetDevice(&dev));
-    SLSP_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    SLSP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, act_row_kernel<IN, KIND, L, QPT>, threads, 0));
-    cap[slot] = sms * (per_sm > 0 ? per_sm : 1);
-  }
-  if (env_row_path() == 1 && a.rows < (int64_t{1} << 31)) {
-    act_row1_kernel<IN, KIND, L, QPT><<<static_cast<unsigned>(a.rows), threads, 0, s>>>(a);
-    SLSP_LAUNCH_CHECK();
-    return SLSP_OK;
-  }
-  const unsigned grid = static_cast<unsigned>(a.rows < cap[slot] ? a.rows : cap[slot]);
-  act_row_kernel<IN, KIND, L, QPT><<<grid, threads, 0, s>>>(a);
+  if (a.rows >= (int64_t{1} << 31)) return SLSP_ERR_UNSUPPORTED;
+  act_row1_kernel<IN, KIND, L, QPT><<<static_cast<unsigned>(a.rows), threads, 0, s>>>(a);
   SLSP_LAUNCH_CHECK();
   return SLSP_OK;
 }
@@ -685,6 +512,8 @@ int launch_row_q(ActArgs& a, int threads, cudaStream_t s) {
 // threads); returns 0 when the caller should use the warp path.
 template <int IN, int KIND, int L>
 int launch_row(ActArgs& a, cudaStream_t s, int* st) {
+  // BF16 input, 6:8 lift or quantize_rows (the hot path); the rest use the warp path
+  if constexpr (IN != IN_BF16 || (L != 8 && L != 4)) return 0;
   using G = WarpGeom<IN, KIND, L>;
   const int64_t nquads = a.cols / G::ELEMS;
   // >= 64 input bytes per thread in flight (a quad is 4L elements), <= 1024 threads
@@ -728,8 +557,6 @@ int try_warp_path(ActArgs& a, cudaStream_t s, int* st) {
   if ((reinterpret_cast<uintptr_t>(a.x) & 15u) || (reinterpret_cast<uintptr_t>(a.out) & 15u)) return 0;
   if (a.cols % (4 * a.l) != 0 || (a.cols * esz) % 16 != 0 || a.out_bytes % 16 != 0) return 0;
   if (a.words_real * 4 * oesz > a.out_bytes) return 0;
-  if constexpr (IN == IN_BF16 && KIND != K_NONE)
-    if (a.l == 8 && env_row_path() == 3 && launch_vec<KIND, 1>(a, s, st)) return 1;
   const bool row = env_row_path() != 0;
   switch (a.l) {
     case 6: return (row && launch_row<IN, KIND, 6>(a, s, st)) || (*st = launch_warp<IN, KIND, 6>(a, s), 1);
@@ -748,8 +575,6 @@ int try_warp_identity(ActArgs& a, cudaStream_t s, int* st) {
   if (a.rows == 0) return 0;
   if ((reinterpret_cast<uintptr_t>(a.x) & 15u) || (reinterpret_cast<uintptr_t>(a.out) & 15u)) return 0;
   if (a.cols % 16 != 0 || (a.cols * esz) % 16 != 0 || a.out_bytes % 16 != 0) return 0;
-  if constexpr (IN == IN_BF16 && KIND != K_NONE)
-    if (env_row_path() == 3 && launch_vec<KIND, 0>(a, s, st)) return 1;
   if (env_row_path() && launch_row<IN, KIND, 4>(a, s, st)) return 1;
   *st = launch_warp<IN, KIND, 4>(a, s);
   return 1;

@@ -349,6 +349,33 @@ __global__ void __launch_bounds__(256) pack68_kernel(const uint8_t* __restrict__
 
 // Row-major 2-bit codes -> MMA-tiled metadata (see slsp_tile_meta in the
 // header): one 16-byte chunk per thread, coalesced on the tiled side.
+// F16 (16-bit A, kind::f16) variant: the 2 KB metadata atom of 128 rows x
+// 128 logical k is CUTLASS's TensorEAtom_MMA_F16 ((8,2,8),(16,2,4)) :
+// ((128,16,2048),(1,1024,32)) in logical elements, 8 per byte — the 8-bit
+// kinds' row-major atom with byte-offset bits 1 and 7 exchanged (row bit 3 <->
+// bit 1 of the byte within the row's 16). One destination chunk per thread,
+// gathered from rows r and r^8 of the row-major codes.
+__global__ void tile_meta_f16_kernel(const uint8_t* __restrict__ meta, int64_t rows, int64_t kp, uint8_t* tiled) {
+  const int64_t ld = kp / 8;
+  const int64_t chunks_per_block = kp / 128;  // 128-logical atoms per 128-row block
+  const int64_t total = (rows + 127) / 128 * 128 * ld / 16;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t rd = i & 127;   // destination row slot within the atom
+    const int64_t at = i >> 7;    // b * chunks_per_block + c
+    const int64_t b = at / chunks_per_block, c = at % chunks_per_block;
+    uint8_t out[16];
+#pragma unroll
+    for (int jd = 0; jd < 16; ++jd) {
+      const int64_t rs = (rd & ~int64_t{8}) | (static_cast<int64_t>((jd >> 1) & 1) << 3);
+      const int js = (jd & ~2) | static_cast<int>(((rd >> 3) & 1) << 1);
+      const int64_t row = b * 128 + rs;
+      out[jd] = row < rows ? meta[row * ld + c * 16 + js] : 0x44;
+    }
+    reinterpret_cast<uint4*>(tiled)[i] = *reinterpret_cast<const uint4*>(out);
+  }
+}
+
 __global__ void tile_meta_kernel(const uint8_t* __restrict__ meta, int64_t rows, int64_t kp, uint8_t* tiled) {
   const int64_t ld = kp / 8;
   const int64_t stages = kp / 256;
@@ -568,6 +595,10 @@ int slsp_gemm_order(int dtype, const void* values, const uint8_t* codes, int64_t
 int64_t slsp_tiled_meta_bytes(int64_t rows, int64_t kp) { return (rows + 127) / 128 * 128 * (kp / 8); }
 
 int slsp_tile_meta(const uint8_t* meta, int64_t rows, int64_t kp, uint8_t* tiled, slsp_stream_t stream) {
+  return slsp_tile_meta_ex(meta, rows, kp, SLSP_DT_I8, tiled, stream);
+}
+
+int slsp_tile_meta_ex(const uint8_t* meta, int64_t rows, int64_t kp, int dtype, uint8_t* tiled, slsp_stream_t stream) {
   using namespace slsp_host;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (rows < 0 || kp <= 0 || !meta || !tiled) return SLSP_ERR_INVALID;
@@ -577,7 +608,8 @@ int slsp_tile_meta(const uint8_t* meta, int64_t rows, int64_t kp, uint8_t* tiled
   if ((st = require_sm100())) return st;
   const int64_t chunks = slsp_tiled_meta_bytes(rows, kp) / 16;
   if (chunks == 0) return SLSP_OK;
-  tile_meta_kernel<<<grid_for(chunks, 256), 256, 0, s>>>(meta, rows, kp, tiled);
+  if (dtype == SLSP_DT_BF16) tile_meta_f16_kernel<<<grid_for(chunks, 256), 256, 0, s>>>(meta, rows, kp, tiled);
+  else tile_meta_kernel<<<grid_for(chunks, 256), 256, 0, s>>>(meta, rows, kp, tiled);
   SLSP_LAUNCH_CHECK();
   return SLSP_OK;
 }

@@ -150,3 +150,25 @@ def test_full_shape_sparse_equals_dense(slsp):
     ys = slsp.sparse_gemm(pw, payload)
     yd = slsp.dense_gemm(w, q.view(torch.int8))
     assert torch.equal(ys, yd)
+
+
+@pytest.mark.parametrize("n,k,m", [(512, 1024, 448), (300, 2048, 64), (768, 4096, 1)])
+def test_sparse_bf16_within_tolerance(slsp, n, k, m):
+    """BF16 6:8 weights (kind::f16 .sp, one metadata column per K=32 MMA) and
+    lifted BF16 activations (lift_row, quantize.hpp:72-89) vs a float64
+    reference of W @ X^T (sparse_gemm<T>, gemm.hpp:164-197, accumulates in
+    double). Stated tolerance: |err| <= 2^-14 * sum|w*x| per output (bf16
+    products are exact in fp32; the bound covers fp32 accumulation)."""
+    g = torch.Generator(device="cuda").manual_seed(n + k + m)
+    w = slsp.magnitude_prune((torch.rand(n, k, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16), 6, 8)
+    x = (torch.rand(m, k, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    pw = slsp.pack_compress(w, 6, 8)
+    lifted = slsp.lift_rows(x, 6, 8, kp=pw.kp)
+    got = slsp.sparse_gemm(pw, lifted).double().cpu()
+    wd, xd = w.double().cpu(), x.double().cpu()
+    want = wd @ xd.T
+    absum = wd.abs() @ xd.abs().T
+    assert torch.all((got - want).abs() <= 2.0 ** -14 * absum + 1e-30)
+    # the same-precision dense kernel agrees to the same bound
+    yd = slsp.dense_gemm(w, x).double().cpu()
+    assert torch.all((yd - want).abs() <= 2.0 ** -14 * absum + 1e-30)
