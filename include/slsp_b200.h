@@ -190,6 +190,21 @@ SLSP_API int slsp_sparse_gemm_x(int dtype, const void* values, const uint8_t* me
                        int64_t m, const float* s_ch, const float* s_tok, int out_mode, void* out, int64_t ldo,
                        slsp_stream_t stream);
 
+/* Workspace of the *_ws GEMM variants: 8*n*m*4 bytes for decode-shaped M
+ * (m <= 256), else 0. With it, GEMMs whose tiles do not fill the 148 SMs
+ * split K across CTAs (up to ws_bytes / (n*m*4) slices, <= 16): each slice
+ * stores its raw int32/fp32 partial sums, a finishing kernel sums the slices
+ * in slice order (exact for INT8, so results stay bit-identical;
+ * deterministic for FP8/BF16) and applies the same epilogue. Stream-ordered;
+ * the workspace must not be shared by concurrent calls. */
+SLSP_API int64_t slsp_gemm_workspace_bytes(int64_t n, int64_t m);
+SLSP_API int slsp_sparse_gemm_ws(int dtype, const void* values, const uint8_t* meta, int64_t n, int64_t kp, const void* act,
+                        int64_t m, const float* s_ch, const float* s_tok, int out_mode, void* out, int64_t ldo,
+                        void* workspace, int64_t ws_bytes, slsp_stream_t stream);
+SLSP_API int slsp_dense_gemm_ws(int dtype, const void* w, int64_t n, int64_t k, const void* act, int64_t m,
+                       const float* s_ch, const float* s_tok, int out_mode, void* out, int64_t ldo, void* workspace,
+                       int64_t ws_bytes, slsp_stream_t stream);
+
 /* a15 — gemm.hpp:142-162 dense_gemm on tcgen05.mma (the speedup
  * denominator). w: n x k, act: m x k (token rows; the reference's X is k x m,
  * the C++ shim transposes), k % 128 == 0. Outputs as slsp_sparse_gemm. */

@@ -102,6 +102,9 @@ def lib() -> C.CDLL:
                 "slsp_lift_rows": (i32, [i32, vp, i64, i64, i32, i32, i64, vp, vp]),
                 "slsp_sparse_gemm": (i32, [i32, vp, vp, i64, i64, vp, i64, vp, vp, i32, vp, i64, vp]),
                 "slsp_dense_gemm": (i32, [i32, vp, i64, i64, vp, i64, vp, vp, i32, vp, i64, vp]),
+                "slsp_sparse_gemm_ws": (i32, [i32, vp, vp, i64, i64, vp, i64, vp, vp, i32, vp, i64, vp, i64, vp]),
+                "slsp_dense_gemm_ws": (i32, [i32, vp, i64, i64, vp, i64, vp, vp, i32, vp, i64, vp, i64, vp]),
+                "slsp_gemm_workspace_bytes": (i64, [i64, i64]),
                 "slsp_tile_meta": (i32, [vp, i64, i64, vp, vp]),
                 "slsp_tile_meta_ex": (i32, [vp, i64, i64, i32, vp, vp]),
                 "slsp_gemm_order": (i32, [i32, vp, vp, i64, i64, i64, vp, vp, i64, vp]),
@@ -379,6 +382,15 @@ def _gemm_out(out_mode: int, n: int, m: int, acc_int: bool, device, out: torch.T
     return torch.empty((m, n), dtype=torch.bfloat16, device=device)
 
 
+def _workspace(n: int, m: int, out_mode: int, device):
+    """Split-K partial-sum slices for decode-shaped GEMMs (stream-ordered
+    caching-allocator memory, one buffer per call)."""
+    nb = int(lib().slsp_gemm_workspace_bytes(n, m))
+    if nb == 0:
+        return None, 0
+    return torch.empty(nb, dtype=torch.uint8, device=device), nb
+
+
 def sparse_gemm(w: PackedWeights, act: torch.Tensor, s_ch: torch.Tensor | None = None,
                 s_tok: torch.Tensor | None = None, out_mode: int = OUT_RAW_NM,
                 out: torch.Tensor | None = None) -> torch.Tensor:
@@ -389,8 +401,10 @@ def sparse_gemm(w: PackedWeights, act: torch.Tensor, s_ch: torch.Tensor | None =
         raise DimensionMismatchError("lifted activation width does not match compressed weights")
     o = _gemm_out(out_mode, w.n, m, w.values.dtype == torch.int8, act.device, out)
     ldo = o.shape[1]
-    _check(lib().slsp_sparse_gemm(w.dtype, _ptr(_raw(w.values)), _ptr(w.tiled()), w.n, w.kp, _ptr(act), m, _ptr(s_ch),
-                                  _ptr(s_tok), out_mode, _ptr(o), ldo, _stream(act.device)), "sparse_gemm")
+    ws, wsb = _workspace(w.n, m, out_mode, act.device)
+    _check(lib().slsp_sparse_gemm_ws(w.dtype, _ptr(_raw(w.values)), _ptr(w.tiled()), w.n, w.kp, _ptr(act), m,
+                                     _ptr(s_ch), _ptr(s_tok), out_mode, _ptr(o), ldo, _ptr(ws), wsb,
+                                     _stream(act.device)), "sparse_gemm")
     return o
 
 
@@ -423,8 +437,9 @@ def dense_gemm(w: torch.Tensor, act: torch.Tensor, s_ch: torch.Tensor | None = N
         raise DimensionMismatchError("dense_gemm: W.cols must equal X.rows")
     o = _gemm_out(out_mode, n, m, w.dtype == torch.int8, act.device, out)
     ldo = o.shape[1]
-    _check(lib().slsp_dense_gemm(dtype_code(w), _ptr(_raw(w)), n, k, _ptr(act), m, _ptr(s_ch), _ptr(s_tok),
-                                 out_mode, _ptr(o), ldo, _stream(act.device)), "dense_gemm")
+    ws, wsb = _workspace(n, m, out_mode, act.device)
+    _check(lib().slsp_dense_gemm_ws(dtype_code(w), _ptr(_raw(w)), n, k, _ptr(act), m, _ptr(s_ch), _ptr(s_tok),
+                                    out_mode, _ptr(o), ldo, _ptr(ws), wsb, _stream(act.device)), "dense_gemm")
     return o
 
 

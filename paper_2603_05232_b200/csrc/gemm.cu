@@ -160,6 +160,14 @@ struct Params {
   unsigned long long* trace;  // perf probing: per-tile clock64 stamps of CTA 0 (env SLSP_GEMM_TRACE = device ptr)
   uint32_t hints;     // kHint* L2 policies
   int group;          // weight tiles per raster band
+  // split-K (decode-shaped M): each (weight tile, token tile) is cut into
+  // ksplit k-ranges; slice s stores its raw partial accumulators (int32 /
+  // fp32) into ws[s][n][m] and a finishing kernel sums the slices in order
+  // (deterministic; exact for int32) and applies the epilogue. ksplit == 1:
+  // the normal epilogue.
+  int ksplit;
+  void* ws;
+  int64_t ws_cap;  // workspace bytes (bounds ksplit)
 };
 
 // Perf probing: slot `slot` of tile iteration `it` on CTA 0 (16 slots per tile;
@@ -172,7 +180,11 @@ struct Params {
 // Raster: bands of `group` weight tiles; within a band the weight tile varies
 // fastest, so the clusters running concurrently share activation tiles (B)
 // and each band's weight tiles stay L2-resident while the band sweeps tokens.
-SLSP_DEVINL void tile_coords(int tile, const Params& p, int m_count, int& mt, int& nt) {
+SLSP_DEVINL void tile_coords(int tile, const Params& p, int m_count, int& mt, int& nt, int& kb0, int& kb1) {
+  const int ks = tile % p.ksplit;  // split-K slice (innermost: the slices of a tile run concurrently)
+  tile /= p.ksplit;
+  kb0 = ks * p.num_kb / p.ksplit;
+  kb1 = (ks + 1) * p.num_kb / p.ksplit;
   const int per_group = p.group * p.n_tiles;
   const int g = tile / per_group;
   const int first = g * p.group;
@@ -393,7 +405,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   const int cluster_id = blockIdx.x / C::CL;
   const int num_clusters = gridDim.x / C::CL;
   const int m_super = (p.m_tiles + C::NPAIR - 1) / C::NPAIR;  // weight tiles per cluster step
-  const int num_tiles = m_super * p.n_tiles;
+  const int num_tiles = m_super * p.n_tiles * p.ksplit;
 
 #ifdef SLSP_WATCHDOG
   if (threadIdx.x == 0 && blockIdx.x < 2)
@@ -440,14 +452,14 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       const uint64_t pol_a = (p.hints & kHintAFirst) ? policy_evict_first() : policy_evict_normal();
       int it = 0;
       for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
-        int ms, nt;
-        tile_coords(tile, p, m_super, ms, nt);
+        int ms, nt, kb0, kb1;
+        tile_coords(tile, p, m_super, ms, nt, kb0, kb1);
         int mt = ms * C::NPAIR + static_cast<int>(pair);
         if (same) mt = nt = 0;
         long long wait_cycles = 0;
         const int a_row = mt * C::BM + static_cast<int>(rank) * C::A_ROWS;
         const int b_row = nt * C::BN + static_cast<int>(rank) * C::B_ROWS;
-        for (int kb = 0; kb < p.num_kb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           const int kl = same ? 0 : kb;
           if (p.trace) {
             const long long t0 = clock64();
@@ -517,6 +529,8 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       int it = 0;
       const uint16_t all_ctas = static_cast<uint16_t>((1u << C::CL) - 1);
       for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
+        int ms_, nt_, kb0, kb1;
+        tile_coords(tile, p, m_super, ms_, nt_, kb0, kb1);
         const int acc = C::ACC_STAGES == 2 ? (it & 1) : 0;
         const uint32_t acc_phase = C::ACC_STAGES == 2 ? ((it >> 1) & 1) : (it & 1);
         // MSUB=1: double-buffered accumulators, tempty[acc]. MSUB=2: one
@@ -543,7 +557,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
           }
 #pragma unroll
           for (int j = 0; j < C::MMAS; ++j) {
-            const uint32_t acc_flag = (kb | j) != 0;
+            const uint32_t acc_flag = (kb != kb0 || j != 0) ? 1u : 0u;
             const uint64_t adesc = smem_desc(a_base + j * 32, 16, 8 * C::A_ROW, C::A_LAYOUT);
             const uint32_t d = d_tmem + h * C::ACC_COLS;
             if constexpr (C::SPARSE) {
@@ -563,7 +577,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         bool sub1_ready = C::MSUB == 1;
         long long wait_cycles = 0;
         int lag = 0, lag_stage = 0, lag_kb = 0;  // deferred subtile-1 k-blocks (consecutive ring stages)
-        for (int kb = 0; kb < p.num_kb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           if (p.trace) {
             const long long t0 = clock64();
             mbar_wait(&full[stage], phase);
@@ -587,7 +601,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
             }
             // catch up once subtile 1 is drained; block when the ring is
             // exhausted or the tile's k-loop ends
-            if (lag == C::STAGES || kb == p.num_kb - 1 || mbar_test(&tempty[1], acc_phase ^ 1)) {
+            if (lag == C::STAGES || kb == kb1 - 1 || mbar_test(&tempty[1], acc_phase ^ 1)) {
               mbar_wait(&tempty[1], acc_phase ^ 1);
               tc_fence_after();
               SLSP_TRACE(it, 1);
@@ -702,8 +716,8 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     const int nch = ncols / 16;
     int it = 0;
     for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
-      int ms, nt;
-      tile_coords(tile, p, m_super, ms, nt);
+      int ms, nt, kb0_, kb1_;
+      tile_coords(tile, p, m_super, ms, nt, kb0_, kb1_);
       const int mt = ms * C::NPAIR + static_cast<int>(pair);
       const int64_t tcol0 = static_cast<int64_t>(nt) * C::BN + half * C::H0;
       const int64_t rowq = static_cast<int64_t>(mt) * C::BM + rank * C::A_ROWS + quarter * 32;  // lane 0's row
@@ -798,8 +812,8 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     int buf = 0;
     int it = 0;
     for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
-      int ms, nt;
-      tile_coords(tile, p, m_super, ms, nt);
+      int ms, nt, kb0_, kb1_;
+      tile_coords(tile, p, m_super, ms, nt, kb0_, kb1_);
       const int mt = ms * C::NPAIR + static_cast<int>(pair);
       const int acc = C::ACC_STAGES == 2 ? (it & 1) : 0;
       const uint32_t acc_phase = C::ACC_STAGES == 2 ? ((it >> 1) & 1) : (it & 1);
@@ -820,6 +834,23 @@ __global__ void __launch_bounds__(C::THREADS, 1)
           uint32_t r[C::EPI_COLS];
           tmem_ld_cols(t_base + c * C::EPI_COLS, r);
           tmem_ld_wait();
+          if (p.ksplit > 1) {  // split-K: this slice's raw partial sums -> ws[slice][row][t]
+            const int64_t row = row0 + lane;
+            if (row < p.n && !(p.debug & kDbgNoStore)) {
+              uint32_t* dst = static_cast<uint32_t*>(p.ws) + (static_cast<int64_t>(tile % p.ksplit) * p.n + row) * p.m + t0;
+              const int64_t valid = imin64(C::EPI_COLS, p.m - t0);
+              if (valid == C::EPI_COLS && (p.m & 3) == 0) {
+#pragma unroll
+                for (int i = 0; i < C::EPI_COLS; i += 4)
+                  *reinterpret_cast<uint4*>(dst + i) = make_uint4(r[i], r[i + 1], r[i + 2], r[i + 3]);
+              } else {
+#pragma unroll
+                for (int i = 0; i < C::EPI_COLS; ++i)
+                  if (i < valid) dst[i] = r[i];
+              }
+            }
+            continue;
+          }
           if (p.tma_store) {
             if (lane == 0) bulk_wait_read<C::EPI_BUFS - 1>();  // staging buffer free again
             __syncwarp();
@@ -965,6 +996,52 @@ int num_sms() {
   return sms;
 }
 
+// Split-K factor for decode-shaped M: the S minimising ceil(tiles*S/clusters)/S
+// (waves per unit of per-tile work; S = 1 unless a split strictly helps), at
+// most `cap` (workspace slices) and at least 2 k-blocks per slice. Env
+// SLSP_GEMM_KSPLIT forces it (within the same bounds).
+int choose_ksplit(int tiles, int num_kb, int clusters, int cap) {
+  const int hi = cap < num_kb / 2 ? cap : num_kb / 2;
+  const int forced = static_cast<int>(env_knob("SLSP_GEMM_KSPLIT", 0));
+  if (forced > 0) return forced < hi ? forced : (hi > 1 ? hi : 1);
+  int best = 1;
+  double best_cost = static_cast<double>((tiles + clusters - 1) / clusters);
+  for (int sp = 2; sp <= hi; ++sp) {
+    const double cost = static_cast<double>((tiles * sp + clusters - 1) / clusters) / sp;
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best = sp;
+    }
+  }
+  return best;
+}
+
+// After a split-K GEMM: sum the slices in slice order (exact for int32,
+// deterministic for fp32), then the epilogue's exact arithmetic — a18 for
+// BF16 outputs (bf16((acc * s_ch[n]) * s_tok[t])), the raw sum for RAW_NM.
+template <typename Acc, int OUT>
+__global__ void splitk_finish_kernel(const Acc* __restrict__ ws, int slices, int64_t n, int64_t m,
+                                     const float* __restrict__ s_ch, const float* __restrict__ s_tok, void* out,
+                                     int64_t ldo) {
+  const int64_t total = n * m;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    Acc acc = ws[i];
+    for (int sl = 1; sl < slices; ++sl) acc += ws[sl * total + i];
+    const int64_t row = i / m, t = i - row * m;
+    if constexpr (OUT == SLSP_OUT_RAW_NM) {
+      static_cast<Acc*>(out)[row * ldo + t] = acc;
+    } else {
+      uint32_t raw;
+      if constexpr (std::is_same<Acc, int32_t>::value) raw = static_cast<uint32_t>(acc);
+      else raw = __float_as_uint(acc);
+      const __nv_bfloat16 b = __float2bfloat16_rn(dequant<Acc>(raw, s_ch[row], s_tok[t]));
+      static_cast<uint16_t*>(out)[OUT == SLSP_OUT_BF16_MN ? t * ldo + row : row * ldo + t] =
+          *reinterpret_cast<const uint16_t*>(&b);
+    }
+  }
+}
+
 template <typename C>
 int run(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const CUtensorMap& o, Params p,
         cudaStream_t s) {
@@ -990,14 +1067,30 @@ int run(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const 
   }
   p.m_tiles = static_cast<int>((p.n + C::BM - 1) / C::BM);
   p.n_tiles = static_cast<int>((p.m + C::BN - 1) / C::BN);
-  const int tiles = (p.m_tiles + C::NPAIR - 1) / C::NPAIR * p.n_tiles;
+  int tiles = (p.m_tiles + C::NPAIR - 1) / C::NPAIR * p.n_tiles;
   if (tiles == 0) return SLSP_OK;
   int clusters = max_clusters;
   const int cluster_cap = static_cast<int>(env_knob("SLSP_GEMM_CLUSTERS", 0));  // perf probing
   if (cluster_cap > 0 && clusters > cluster_cap) clusters = cluster_cap;
+  // split-K where the tiles do not fill the machine (decode-shaped M): needs
+  // an accumulation target (the int32/fp32 output itself, or a workspace)
+  p.ksplit = 1;
+  if constexpr (!C::REG_EPI && !C::LIFT) {
+    const int64_t slice = p.n * p.m * 4;
+    const int cap = p.ws && slice > 0 ? static_cast<int>(p.ws_cap / slice < 16 ? p.ws_cap / slice : 16) : 1;
+    if (p.m <= 256 && cap > 1) p.ksplit = choose_ksplit(tiles, p.num_kb, clusters, cap);
+  }
+  if (p.ksplit > 1) tiles *= p.ksplit;
   if (clusters > tiles) clusters = tiles;
   cfg.gridDim = dim3(C::CL * clusters);
   SLSP_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, a, b, e, o, p));
+  if (p.ksplit > 1) {
+    const int64_t total = p.n * p.m;
+    const unsigned grid = static_cast<unsigned>((total + 255) / 256 < 148 * 16 ? (total + 255) / 256 : 148 * 16);
+    splitk_finish_kernel<typename C::Acc, C::OUT><<<grid, 256, 0, s>>>(
+        static_cast<const typename C::Acc*>(p.ws), p.ksplit, p.n, p.m, p.s_ch, p.s_tok, p.out, p.ldo);
+    SLSP_CUDA_TRY(cudaGetLastError());
+  }
   return SLSP_OK;
 }
 
@@ -1012,19 +1105,22 @@ int run_out_cl(int out_mode, const CUtensorMap& a, const CUtensorMap& b, const C
   return SLSP_ERR_INVALID;
 }
 
-// Tile shape knobs: 1 or 2 M-subtiles per CTA pair (env SLSP_GEMM_MSUB for
-// the sparse kernel, SLSP_DGEMM_MSUB for the dense one); SLSP_GEMM_EPIW=32
-// forces 32-column epilogue chunks for one-subtile tiles (perf probing).
+// Tile shape: 1 or 2 M-subtiles per CTA pair (env SLSP_GEMM_MSUB for the
+// sparse kernel, SLSP_DGEMM_MSUB for the dense one; decode tiles: 1).
 template <bool SPARSE, MmaKind K, int BN, int LIFT = 0>
 int run_out(int out_mode, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const CUtensorMap& o,
-            const Params& p, cudaStream_t s, uint32_t msub, uint32_t ew) {
-  if (msub == 2) return run_out_cl<SPARSE, K, BN, 2, LIFT, 0>(out_mode, a, b, e, o, p, s);
-  if (!LIFT && ew == 32) return run_out_cl<SPARSE, K, BN, 1, 0, 32>(out_mode, a, b, e, o, p, s);
+            const Params& p, cudaStream_t s, uint32_t msub) {
+  if constexpr (BN >= 128)
+    if (msub == 2) return run_out_cl<SPARSE, K, BN, 2, LIFT, 0>(out_mode, a, b, e, o, p, s);
   return run_out_cl<SPARSE, K, BN, 1, LIFT, 0>(out_mode, a, b, e, o, p, s);
 }
 
 constexpr int kSparseBN = 224;
 constexpr int kDenseBN = 256;
+// Decode-shaped M (<= 64 tokens): 64-token tiles, so the smem ring holds
+// mostly weight bytes (8 stages instead of 4) for the HBM-bound weight stream.
+constexpr int kDecodeBN = 64;
+constexpr int64_t kDecodeM = 64;
 constexpr uint32_t kDenseMsub = 1;
 constexpr uint32_t kRasterGroup = 16;  // measured best of {4, 8, 16, 32, 148} on Qwen2.5-7B shapes
 
@@ -1033,13 +1129,10 @@ constexpr uint32_t kRasterGroup = 16;  // measured best of {4, 8, 16, 32, 148} o
 // tile count; use them unless that leaves a partial last wave the one-subtile
 // grid would not have (measured on Qwen2.5-7B shapes).
 uint32_t sparse_msub(int64_t n, int64_t m) {
-  const int64_t clusters = num_sms() / 2;
-  const int64_t nt = (m + kSparseBN - 1) / kSparseBN;
-  const int64_t t1 = (n + 255) / 256 * nt, t2 = (n + 511) / 512 * nt;
-  const int64_t w1 = (t1 + clusters - 1) / clusters, w2 = (t2 + clusters - 1) / clusters;
-  // per-tile cost of a 2-subtile tile ~ 1.9x a 1-subtile tile
-  return 19 * w2 <= 10 * w1 ? 2u : 1u;
+  if (m <= 256) return 1;  // decode shapes: more weight tiles (split-K runs on one-subtile tiles)
+  return 2;  // measured faster or equal on every Qwen2.5-7B shape at M >= 2048
 }
+
 
 int check_out(int out_mode, const float* s_ch, const float* s_tok, void* out, int64_t ldo, int64_t n, int64_t m) {
   if (!out) return SLSP_ERR_INVALID;
@@ -1060,7 +1153,7 @@ int check_out(int out_mode, const float* s_ch, const float* s_tok, void* out, in
 template <bool LIFT>
 int sparse_entry(int dtype, const void* values, const uint8_t* meta, int64_t n, int64_t kp, const void* act,
                  int64_t act_row, int64_t m, const float* s_ch, const float* s_tok, int out_mode, void* out,
-                 int64_t ldo, slsp_stream_t stream) {
+                 int64_t ldo, slsp_stream_t stream, void* ws = nullptr, int64_t ws_bytes = 0) {
   using namespace slsp_host;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (n < 0 || m < 0 || kp <= 0) return SLSP_ERR_INVALID;
@@ -1076,14 +1169,17 @@ int sparse_entry(int dtype, const void* values, const uint8_t* meta, int64_t n, 
   CUtensorMap ta, tb, te, to;
   Params p{};
   if ((st = make_map_2d(&ta, values, kp / 2 * esz, n, 128))) return st;
-  const uint32_t msub = env_knob("SLSP_GEMM_MSUB", sparse_msub(n, m)) == 2 ? 2 : 1;
-  const uint32_t ew = LIFT ? 0 : env_knob("SLSP_GEMM_EPIW", 0);
-  if ((st = make_map_2d(&tb, act, act_row * esz, m, kSparseBN / 2))) return st;
+  const bool decode = !LIFT && m <= kDecodeM;
+  const int bn = decode ? kDecodeBN : kSparseBN;
+  const uint32_t msub = decode ? 1u : env_knob("SLSP_GEMM_MSUB", sparse_msub(n, m)) == 2 ? 2u : 1u;
+  if (ws && ws_bytes >= 2 * n * m * 4) {  // split-K partial-sum slices
+    p.ws = ws;
+    p.ws_cap = ws_bytes;
+  }
+  if ((st = make_map_2d(&tb, act, act_row * esz, m, bn / 2))) return st;
   // BF16: a 128-byte A stage is 128 logical k -> one 2 KB metadata atom per stage
   if ((st = make_map_meta(&te, meta, n, kp, esz == 2 ? 8 : 16))) return st;
-  if ((st = make_map_out(&to, out, out_mode, n, m, ldo, ew == 32 && msub == 1 ? 32 : epi_cols(msub, kSparseBN, out_mode),
-                         &p.tma_store)))
-    return st;
+  if ((st = make_map_out(&to, out, out_mode, n, m, ldo, epi_cols(msub, bn, out_mode), &p.tma_store))) return st;
   select_epilogue(p, out_mode, msub, out, ldo, s_tok);
   p.n = n;
   p.m = m;
@@ -1097,10 +1193,16 @@ int sparse_entry(int dtype, const void* values, const uint8_t* meta, int64_t n, 
   p.hints = env_knob("SLSP_GEMM_HINTS", kDefaultHints);
   p.group = static_cast<int>(env_knob("SLSP_GEMM_GROUP", kRasterGroup));
   constexpr int L = LIFT ? 1 : 0;
-  if (dtype == SLSP_DT_I8) return run_out<true, MmaKind::I8, kSparseBN, L>(out_mode, ta, tb, te, to, p, s, msub, ew);
-  if constexpr (!LIFT)
-    if (dtype == SLSP_DT_BF16) return run_out<true, MmaKind::F16, kSparseBN>(out_mode, ta, tb, te, to, p, s, msub, ew);
-  return run_out<true, MmaKind::F8, kSparseBN, L>(out_mode, ta, tb, te, to, p, s, msub, ew);
+  if constexpr (!LIFT) {
+    if (decode) {
+      if (dtype == SLSP_DT_I8) return run_out<true, MmaKind::I8, kDecodeBN>(out_mode, ta, tb, te, to, p, s, 1);
+      if (dtype == SLSP_DT_BF16) return run_out<true, MmaKind::F16, kDecodeBN>(out_mode, ta, tb, te, to, p, s, 1);
+      return run_out<true, MmaKind::F8, kDecodeBN>(out_mode, ta, tb, te, to, p, s, 1);
+    }
+    if (dtype == SLSP_DT_BF16) return run_out<true, MmaKind::F16, kSparseBN>(out_mode, ta, tb, te, to, p, s, msub);
+  }
+  if (dtype == SLSP_DT_I8) return run_out<true, MmaKind::I8, kSparseBN, L>(out_mode, ta, tb, te, to, p, s, msub);
+  return run_out<true, MmaKind::F8, kSparseBN, L>(out_mode, ta, tb, te, to, p, s, msub);
 }
 
 }  // namespace
@@ -1113,6 +1215,15 @@ int slsp_sparse_gemm(int dtype, const void* values, const uint8_t* meta, int64_t
   return sparse_entry<false>(dtype, values, meta, n, kp, act, kp, m, s_ch, s_tok, out_mode, out, ldo, stream);
 }
 
+int slsp_sparse_gemm_ws(int dtype, const void* values, const uint8_t* meta, int64_t n, int64_t kp, const void* act,
+                        int64_t m, const float* s_ch, const float* s_tok, int out_mode, void* out, int64_t ldo,
+                        void* workspace, int64_t ws_bytes, slsp_stream_t stream) {
+  return sparse_entry<false>(dtype, values, meta, n, kp, act, kp, m, s_ch, s_tok, out_mode, out, ldo, stream, workspace,
+                             ws_bytes);
+}
+
+int64_t slsp_gemm_workspace_bytes(int64_t n, int64_t m) { return m <= 256 ? 8 * n * m * 4 : 0; }
+
 int slsp_sparse_gemm_x(int dtype, const void* values, const uint8_t* meta, int64_t n, int64_t kx, const void* act,
                        int64_t m, const float* s_ch, const float* s_tok, int out_mode, void* out, int64_t ldo,
                        slsp_stream_t stream) {
@@ -1123,6 +1234,12 @@ int slsp_sparse_gemm_x(int dtype, const void* values, const uint8_t* meta, int64
 
 int slsp_dense_gemm(int dtype, const void* w, int64_t n, int64_t k, const void* act, int64_t m, const float* s_ch,
                     const float* s_tok, int out_mode, void* out, int64_t ldo, slsp_stream_t stream) {
+  return slsp_dense_gemm_ws(dtype, w, n, k, act, m, s_ch, s_tok, out_mode, out, ldo, nullptr, 0, stream);
+}
+
+int slsp_dense_gemm_ws(int dtype, const void* w, int64_t n, int64_t k, const void* act, int64_t m, const float* s_ch,
+                       const float* s_tok, int out_mode, void* out, int64_t ldo, void* workspace, int64_t ws_bytes,
+                       slsp_stream_t stream) {
   using namespace slsp_host;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (n < 0 || m < 0 || k <= 0) return SLSP_ERR_INVALID;
@@ -1138,10 +1255,15 @@ int slsp_dense_gemm(int dtype, const void* w, int64_t n, int64_t k, const void* 
   CUtensorMap ta, tb, to;
   Params p{};
   if ((st = make_map_2d(&ta, w, k * esz, n, 128))) return st;
-  const uint32_t msub = env_knob("SLSP_DGEMM_MSUB", kDenseMsub) == 2 ? 2 : 1;
-  const uint32_t ew = env_knob("SLSP_GEMM_EPIW", 0);
-  if ((st = make_map_2d(&tb, act, k * esz, m, kDenseBN / 2))) return st;
-  if ((st = make_map_out(&to, out, out_mode, n, m, ldo, ew == 32 && msub == 1 ? 32 : epi_cols(msub, kDenseBN, out_mode), &p.tma_store))) return st;
+  const bool decode = m <= kDecodeM;
+  const int bn = decode ? kDecodeBN : kDenseBN;
+  const uint32_t msub = decode ? 1u : env_knob("SLSP_DGEMM_MSUB", kDenseMsub) == 2 ? 2u : 1u;
+  if (workspace && ws_bytes >= 2 * n * m * 4) {  // split-K partial-sum slices
+    p.ws = workspace;
+    p.ws_cap = ws_bytes;
+  }
+  if ((st = make_map_2d(&tb, act, k * esz, m, bn / 2))) return st;
+  if ((st = make_map_out(&to, out, out_mode, n, m, ldo, epi_cols(msub, bn, out_mode), &p.tma_store))) return st;
   select_epilogue(p, out_mode, msub, out, ldo, s_tok);
   p.n = n;
   p.m = m;
@@ -1155,10 +1277,13 @@ int slsp_dense_gemm(int dtype, const void* w, int64_t n, int64_t k, const void* 
   p.hints = env_knob("SLSP_GEMM_HINTS", kDefaultHints);
   p.group = static_cast<int>(env_knob("SLSP_GEMM_GROUP", kRasterGroup));
   if (dtype == SLSP_DT_I8)
-    return run_out<false, MmaKind::I8, kDenseBN>(out_mode, ta, tb, ta, to, p, s, msub, ew);
+    return decode ? run_out<false, MmaKind::I8, kDecodeBN>(out_mode, ta, tb, ta, to, p, s, 1)
+                  : run_out<false, MmaKind::I8, kDenseBN>(out_mode, ta, tb, ta, to, p, s, msub);
   if (dtype == SLSP_DT_E4M3)
-    return run_out<false, MmaKind::F8, kDenseBN>(out_mode, ta, tb, ta, to, p, s, msub, ew);
-  return run_out<false, MmaKind::F16, kDenseBN>(out_mode, ta, tb, ta, to, p, s, msub, ew);
+    return decode ? run_out<false, MmaKind::F8, kDecodeBN>(out_mode, ta, tb, ta, to, p, s, 1)
+                  : run_out<false, MmaKind::F8, kDenseBN>(out_mode, ta, tb, ta, to, p, s, msub);
+  return decode ? run_out<false, MmaKind::F16, kDecodeBN>(out_mode, ta, tb, ta, to, p, s, 1)
+                : run_out<false, MmaKind::F16, kDenseBN>(out_mode, ta, tb, ta, to, p, s, msub);
 }
 
 }  // extern "C"

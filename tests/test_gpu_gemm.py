@@ -172,3 +172,44 @@ def test_sparse_bf16_within_tolerance(slsp, n, k, m):
     # the same-precision dense kernel agrees to the same bound
     yd = slsp.dense_gemm(w, x).double().cpu()
     assert torch.all((yd - want).abs() <= 2.0 ** -14 * absum + 1e-30)
+
+
+@pytest.mark.parametrize("m", [1, 16, 64])
+def test_decode_split_k_int8_bit_exact(slsp, orc, m):
+    """Decode-shaped M: the tiles do not fill the GPU, so K is split across
+    CTAs and int32 partial sums are added atomically — exact, so the result is
+    still bit-identical to the oracle (gemm.hpp:199-233)."""
+    rng = np.random.default_rng(m)
+    n, k = 1024, 4096
+    w, x, vals, codes, payload, scales, kp = sparse_case(orc, rng, n, k, m)
+    got = run_sparse_raw(slsp, vals, codes, payload, kp, n)
+    assert np.array_equal(got, orc.sparse_gemm_words(vals, codes, payload))
+
+
+@pytest.mark.parametrize("m", [1, 16, 64])
+def test_decode_split_k_bf16_epilogue_identical(slsp, m):
+    """BF16 outputs of a split-K GEMM (workspace + finishing kernel) equal the
+    unsplit GEMM's bit for bit (INT8: same int32 sums, same fp32 epilogue)."""
+    import os
+
+    g = torch.Generator(device="cuda").manual_seed(m)
+    n, k = 2048, 4096
+    w = slsp.magnitude_prune(torch.randint(-127, 128, (n, k), dtype=torch.int8, device="cuda", generator=g), 6, 8)
+    x = (torch.rand(m, k, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    s_ch = torch.rand(n, device="cuda", generator=g) * 0.01 + 0.001
+    pw = slsp.pack_compress(w, 6, 8)
+    payload, s_tok = slsp.fused_quant_slide(x, 6, 8)
+    q, q_s = slsp.quantize_rows(x)
+    outs = {}
+    for ks in ("1", "0"):  # forced unsplit, then the automatic split
+        os.environ["SLSP_GEMM_KSPLIT"] = ks
+        try:
+            for mode in (slsp.OUT_BF16_NM, slsp.OUT_BF16_MN):
+                outs[(ks, mode, "s")] = slsp.sparse_gemm(pw, payload, s_ch=s_ch, s_tok=s_tok, out_mode=mode)
+                outs[(ks, mode, "d")] = slsp.dense_gemm(w, q.view(torch.int8), s_ch=s_ch, s_tok=q_s, out_mode=mode)
+        finally:
+            del os.environ["SLSP_GEMM_KSPLIT"]
+    torch.cuda.synchronize()
+    for mode in (slsp.OUT_BF16_NM, slsp.OUT_BF16_MN):
+        for kind in ("s", "d"):
+            assert torch.equal(outs[("1", mode, kind)].view(torch.int16), outs[("0", mode, kind)].view(torch.int16))
