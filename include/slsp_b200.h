@@ -165,6 +165,19 @@ SLSP_API int slsp_sparse_gemm(int dtype, const void* values, const uint8_t* meta
                      int64_t m, const float* s_ch, const float* s_tok, int out_mode, void* out, int64_t ldo,
                      slsp_stream_t stream);
 
+/* SLSP kind-2 container payload -> MMA-ready weights (
+ * container.hpp:379-390 to_container / :424-435 compressed_from). values:
+ * the container's values section on the device (rows x windows x 2 elements);
+ * codes_stream: its metadata section (2-bit codes, four per byte LSB-first,
+ * container.hpp:330-336, contiguous over the whole matrix). Writes values_out
+ * (rows x kp/2) and meta_out (rows x kp/8, the slsp_pack_compress layout; tile
+ * it with slsp_tile_meta_ex), padding windows = value 0 / codes (0,1).
+ * kp >= 4*windows, kp % 8 == 0 (the GEMM needs kp % 256 == 0). The host side
+ * (file I/O, header, CRC-32, the reference's ContainerError checks) is
+ * paper_2603_05232_b200/container.py. */
+SLSP_API int slsp_load_compressed(int dtype, const void* values, const uint8_t* codes_stream, int64_t rows,
+                         int64_t windows, int64_t kp, void* values_out, uint8_t* meta_out, slsp_stream_t stream);
+
 /* GEMM window order for in-SM lifting (6:8). Permutes the windows of
  * slsp_pack_compress output (values rows x kp_ref/2, row-major codes
  * rows x kp_ref/8; K' = 3*ceil(cols/8)*4 real lifted positions) into the

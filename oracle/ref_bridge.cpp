@@ -343,4 +343,38 @@ void ref_pack_codes(const std::uint8_t* codes, std::int64_t count, std::uint8_t*
   std::memcpy(out, packed.data(), packed.size());
 }
 
+// container.hpp serialize(to_container(CompressedSparseMatrix<int8_t>)) — the
+// reference's kind-2 file bytes (pinning the loader). codes
+// are one 2-bit position per byte (the in-memory format); returns the byte
+// count written, or -needed when cap is too small.
+std::int64_t ref_serialize_compressed_i8(const std::int8_t* values, const std::uint8_t* codes, std::int64_t rows,
+                                         std::int64_t windows, int z, int l, std::uint8_t* out, std::int64_t cap) {
+  CompressedSparseMatrix<std::int8_t> cm;
+  cm.rows = static_cast<std::size_t>(rows);
+  cm.windows_per_row = static_cast<std::size_t>(windows);
+  cm.pattern = SparsityPattern(z, l);
+  cm.values.assign(values, values + rows * windows * 2);
+  cm.metadata.assign(codes, codes + rows * windows * 2);
+  const auto bytes = slsp::serialize(slsp::to_container(cm));
+  if (static_cast<std::int64_t>(bytes.size()) > cap) return -static_cast<std::int64_t>(bytes.size());
+  std::memcpy(out, bytes.data(), bytes.size());
+  return static_cast<std::int64_t>(bytes.size());
+}
+
+// serialize(to_container(QuantizedLiftedActivation)) — a kind-3 file.
+std::int64_t ref_serialize_quantized(const std::uint32_t* payload, const float* scales, std::int64_t rows,
+                                     std::int64_t words, int z, int l, int kind, std::uint8_t* out, std::int64_t cap) {
+  QuantizedLiftedActivation a;
+  a.rows = static_cast<std::size_t>(rows);
+  a.words_per_row = static_cast<std::size_t>(words);
+  a.pattern = SparsityPattern(z, l);
+  a.kind = to_kind(kind);
+  a.payload.assign(payload, payload + rows * words);
+  a.scales.assign(scales, scales + rows);
+  const auto bytes = slsp::serialize(slsp::to_container(a));
+  if (static_cast<std::int64_t>(bytes.size()) > cap) return -static_cast<std::int64_t>(bytes.size());
+  std::memcpy(out, bytes.data(), bytes.size());
+  return static_cast<std::int64_t>(bytes.size());
+}
+
 }  // extern "C"

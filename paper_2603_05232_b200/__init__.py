@@ -12,4 +12,6 @@ from ._native import (  # noqa: F401
     plan_decomposition, quantize_rows, round_up, sparse_gemm, sparse_gemm_x, tile_meta,
 )
 
+from . import container  # noqa: F401,E402
+
 __version__ = "0.1.0"

@@ -107,6 +107,7 @@ def lib() -> C.CDLL:
                 "slsp_gemm_workspace_bytes": (i64, [i64, i64]),
                 "slsp_tile_meta": (i32, [vp, i64, i64, vp, vp]),
                 "slsp_tile_meta_ex": (i32, [vp, i64, i64, i32, vp, vp]),
+                "slsp_load_compressed": (i32, [i32, vp, vp, i64, i64, i64, vp, vp, vp]),
                 "slsp_gemm_order": (i32, [i32, vp, vp, i64, i64, i64, vp, vp, i64, vp]),
                 "slsp_sparse_gemm_x": (i32, [i32, vp, vp, i64, i64, vp, i64, vp, vp, i32, vp, i64, vp]),
                 "slsp_tiled_meta_bytes": (i64, [i64, i64]),

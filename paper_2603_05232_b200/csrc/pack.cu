@@ -437,6 +437,43 @@ __global__ void gemm_order_kernel(const uint8_t* __restrict__ vals, const uint8_
   }
 }
 
+// container.hpp kind-2 payload -> MMA-ready operands: values [rows][W][2]
+// (elem bytes each) -> [rows][kp/2] zero-padded; the codes stream (2-bit codes
+// packed four per byte over the whole matrix, container.hpp:330-336, so a
+// row's windows start at nibble r*W) -> row-major [rows][kp/8] with canonical
+// codes (0,1) for the padding windows. One thread per output metadata byte
+// (two windows) plus its values.
+template <int ESZ>
+__global__ void load_compressed_kernel(const uint8_t* __restrict__ vals, const uint8_t* __restrict__ stream,
+                                       int64_t rows, int64_t W, int64_t kp, uint8_t* __restrict__ vout,
+                                       uint8_t* __restrict__ mout) {
+  const int64_t per_row = kp / 8;  // output metadata bytes per row = windows / 2
+  const int64_t total = rows * per_row;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = t / per_row, b = t - r * per_row;
+    uint32_t byte = 0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t j = 2 * b + h;  // window
+      uint32_t nib = 0x4u;
+      uint8_t* vo = vout + (r * (kp / 2) + 2 * j) * ESZ;
+      if (j < W) {
+        const int64_t q = r * W + j;  // nibble index in the stream
+        nib = (stream[q >> 1] >> (4 * (q & 1))) & 0xFu;
+        const uint8_t* vi = vals + (r * W + j) * 2 * ESZ;
+#pragma unroll
+        for (int e = 0; e < 2 * ESZ; ++e) vo[e] = vi[e];
+      } else {
+#pragma unroll
+        for (int e = 0; e < 2 * ESZ; ++e) vo[e] = 0;
+      }
+      byte |= nib << (4 * h);
+    }
+    mout[t] = static_cast<uint8_t>(byte);
+  }
+}
+
 template <int MODE>
 int launch_pack(int esz, PackArgs& a, cudaStream_t s) {
   const int64_t chunks = (a.group_slots + kThreads - 1) / kThreads;
@@ -588,6 +625,26 @@ int slsp_gemm_order(int dtype, const void* values, const uint8_t* codes, int64_t
   auto* vo = static_cast<uint8_t*>(values_out);
   if (esz == 1) gemm_order_kernel<1><<<grid_for(total, 256), 256, 0, s>>>(v, codes, rows, nblk, kp_ref, vo, codes_out, kp_out);
   else gemm_order_kernel<2><<<grid_for(total, 256), 256, 0, s>>>(v, codes, rows, nblk, kp_ref, vo, codes_out, kp_out);
+  SLSP_LAUNCH_CHECK();
+  return SLSP_OK;
+}
+
+int slsp_load_compressed(int dtype, const void* values, const uint8_t* codes_stream, int64_t rows, int64_t windows,
+                         int64_t kp, void* values_out, uint8_t* meta_out, slsp_stream_t stream) {
+  using namespace slsp_host;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int esz = elem_size(dtype);
+  if ((esz != 1 && esz != 2) || rows < 0 || windows < 0 || !values || !codes_stream || !values_out || !meta_out)
+    return SLSP_ERR_INVALID;
+  if (kp % 8 != 0 || kp / 4 < windows) return SLSP_ERR_DIMENSION;
+  int st;
+  if ((st = require_sm100())) return st;
+  const int64_t total = rows * (kp / 8);
+  if (total == 0) return SLSP_OK;
+  const auto* v = static_cast<const uint8_t*>(values);
+  auto* vo = static_cast<uint8_t*>(values_out);
+  if (esz == 1) load_compressed_kernel<1><<<grid_for(total, 256), 256, 0, s>>>(v, codes_stream, rows, windows, kp, vo, meta_out);
+  else load_compressed_kernel<2><<<grid_for(total, 256), 256, 0, s>>>(v, codes_stream, rows, windows, kp, vo, meta_out);
   SLSP_LAUNCH_CHECK();
   return SLSP_OK;
 }

@@ -65,6 +65,18 @@ def main():
     wp = rng.integers(-127, 128, size=(16, 48)).astype(np.int8)
     pruned = R.magnitude_prune(wp, 6, 8, DT_I8)
     np.savez_compressed(HERE / "codec_prune.npz", xs=xs, enc=enc, dec=dec, wp=wp, pruned=pruned)
+    # --- SLSP containers (container.hpp) written by the reference: kind 2 ----
+    # (compressed weights, even and odd windows per row) and kind 3 (lifted
+    # activations); pin the loader of SURVEY.md §8f #1
+    for tag, rows, groups in (("even", 40, 64), ("odd", 7, 5)):
+        w = compliant_matrix(rng, rows, groups, 6, 8)
+        values, codes = R.compress(R.pack_matrix(w, 6, 8, DT_I8), DT_I8)
+        (HERE / f"container_6_8_{tag}.slsp").write_bytes(R.serialize_compressed_i8(values, codes, 6, 8))
+        np.savez_compressed(HERE / f"container_6_8_{tag}.npz", w=w, values=values, codes=codes)
+    x = rng.uniform(-2, 2, size=(9, 96)).astype(np.float32)
+    payload, scales = R.fused_quant_slide(x, 6, 8, KIND_INT8, DT_F32)
+    (HERE / "container_fqs_6_8.slsp").write_bytes(R.serialize_quantized(payload, scales, 6, 8, KIND_INT8))
+    np.savez_compressed(HERE / "container_fqs_6_8.npz", x=x, payload=payload, scales=scales)
     print("wrote", sorted(p.name for p in HERE.glob("*.npz")))
 
 

@@ -65,6 +65,11 @@ class Oracle:
             fn.restype = res
             fn.argtypes = args
             setattr(self, "_" + name, fn)
+        if prefix == "ref_":  # container.hpp serialization (the reference only)
+            self.lib.ref_serialize_compressed_i8.restype = i64
+            self.lib.ref_serialize_compressed_i8.argtypes = [vp, vp, i64, i64, i32, i32, vp, i64]
+            self.lib.ref_serialize_quantized.restype = i64
+            self.lib.ref_serialize_quantized.argtypes = [vp, vp, i64, i64, i32, i32, i32, vp, i64]
         if prefix == "orc_":
             for name in ("orc_dequant_bf16", "orc_dequant_f32_bf16"):
                 fn = getattr(self.lib, name)
@@ -197,6 +202,25 @@ class Oracle:
         out = np.zeros((codes.size + 3) // 4, dtype=np.uint8)
         self._pack_codes(_p(codes), codes.size, _p(out))
         return out
+
+    # ---- reference-only: container.hpp serialize(to_container(...)) ---------
+    def serialize_compressed_i8(self, values: np.ndarray, codes: np.ndarray, z: int, l: int) -> bytes:
+        rows, wx2 = values.shape
+        values = np.ascontiguousarray(values, dtype=np.int8)
+        codes = np.ascontiguousarray(codes, dtype=np.uint8)
+        out = np.zeros(64 + values.nbytes + codes.size, dtype=np.uint8)
+        n = self.lib.ref_serialize_compressed_i8(_p(values), _p(codes), rows, wx2 // 2, z, l, _p(out), out.size)
+        assert n > 0
+        return out[:n].tobytes()
+
+    def serialize_quantized(self, payload: np.ndarray, scales: np.ndarray, z: int, l: int, kind: int) -> bytes:
+        rows, words = payload.shape
+        payload = np.ascontiguousarray(payload, dtype=np.uint32)
+        scales = np.ascontiguousarray(scales, dtype=np.float32)
+        out = np.zeros(64 + payload.nbytes + scales.nbytes, dtype=np.uint8)
+        n = self.lib.ref_serialize_quantized(_p(payload), _p(scales), rows, words, z, l, kind, _p(out), out.size)
+        assert n > 0
+        return out[:n].tobytes()
 
     # ---- restatement-only: a18 dequant epilogue -----------------------------
     def dequant_bf16(self, acc: np.ndarray, s_ch: np.ndarray, s_tok: np.ndarray) -> np.ndarray:
