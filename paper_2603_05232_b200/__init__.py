@@ -13,5 +13,6 @@ from ._native import (  # noqa: F401
 )
 
 from . import container  # noqa: F401,E402
+from .verify import EquivalenceReport, check_equivalence  # noqa: F401,E402
 
 __version__ = "0.1.0"

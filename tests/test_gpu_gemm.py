@@ -213,3 +213,27 @@ def test_decode_split_k_bf16_epilogue_identical(slsp, m):
     for mode in (slsp.OUT_BF16_NM, slsp.OUT_BF16_MN):
         for kind in ("s", "d"):
             assert torch.equal(outs[("1", mode, kind)].view(torch.int16), outs[("0", mode, kind)].view(torch.int16))
+
+
+@pytest.mark.parametrize("z,l,n,k,m", [(6, 8, 512, 1024, 300), (4, 6, 256, 600, 100), (6, 8, 3584, 3584, 8192)])
+def test_gpu_check_equivalence(slsp, z, l, n, k, m):
+    """gemm.hpp:258-286 on the GPU: dense vs the full sparse pipeline, exact
+    (last case: Qwen2.5-7B o_proj at M=8192)."""
+    g = torch.Generator(device="cuda").manual_seed(n + m)
+    kk = -(-k // l) * l
+    w = slsp.magnitude_prune(torch.randint(-127, 128, (n, kk), dtype=torch.int8, device="cuda", generator=g), z, l)
+    w = w[:, :k].contiguous()
+    x = torch.randint(-127, 128, (k, m), dtype=torch.int8, device="cuda", generator=g)
+    rep = slsp.check_equivalence(w, x, z, l)
+    assert rep.exact and rep.max_abs_diff == 0
+    # op-count ratio = gamma * hw_m / hw_n on whole blocks (acceptance.cpp:335-357)
+    if k % l == 0:
+        wc = (l - 4) // 2 + 1
+        assert rep.sparse_multiplies * l == rep.dense_multiplies * wc * 2
+
+
+def test_gpu_check_equivalence_rejects_noncompliant(slsp):
+    w = torch.ones((128, 64), dtype=torch.int8, device="cuda")
+    x = torch.ones((64, 32), dtype=torch.int8, device="cuda")
+    with pytest.raises(slsp.NotCompliantError, match="row 0, block 0"):
+        slsp.check_equivalence(w, x, 6, 8)
