@@ -9,8 +9,8 @@ from pathlib import Path
 import numpy as np
 import torch
 
-sys.path.insert(0, str(Path(__file__).resolve().parent))
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
 
 import paper_2603_05232_b200 as slsp  # noqa: E402
 from helpers import compliant_matrix, lifted_width, mma_format, pad_cols, round_up  # noqa: E402

@@ -4,7 +4,7 @@ from pathlib import Path
 
 import torch
 
-sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
 import paper_2603_05232_b200 as slsp  # noqa: E402
 
 g = torch.Generator(device="cuda").manual_seed(0)
