@@ -51,7 +51,7 @@ constexpr int epi_cols(int msub, int bn, int out) {
   return msub == 2 ? (out == SLSP_OUT_BF16_NM ? 32 : 16) : (out == SLSP_OUT_RAW_NM || bn % 64 != 0) ? 32 : 64;
 }
 
-template <bool SPARSE_, MmaKind KIND_, int BN_, int STAGES_, int OUT_, int MSUB_ = 1, int LIFT_ = 0, int EW_ = 0>
+template <bool SPARSE_, MmaKind KIND_, int BN_, int STAGES_, int OUT_, int MSUB_ = 1, int LIFT_ = 0, int KH_ = 0>
 struct Cfg {
   static constexpr bool SPARSE = SPARSE_;
   static constexpr MmaKind KIND = KIND_;
@@ -83,24 +83,30 @@ struct Cfg {
   static constexpr int A_ROWS = 128;      // per CTA per M-subtile
   static constexpr int B_ROWS = BN / 2;   // tokens per CTA
   static_assert(!LIFT || B_ROWS % (8 * (LIFT ? LIFT_WARPS : 1)) == 0, "lift warps own whole 8-row swizzle groups");
-  static constexpr int A_ROW = 128;                          // A bytes per row per stage
-  static constexpr uint32_t A_LAYOUT = 2u;                   // UMMA desc: SWIZZLE_128B
+  // Half k-stages (sparse 8-bit kinds): 128 lifted bytes per stage instead of
+  // 256 — A rows of 64 B (64B swizzle), one B atom, one metadata atom, 2 MMAs
+  // per subtile — so the same ring holds twice as many, half-size stages
+  // (6 x 34 KB for MSUB=2 instead of 3 x 68 KB): more latency cover per byte.
+  static constexpr bool KH = KH_ != 0;
+  static_assert(!KH || (SPARSE && KIND != MmaKind::F16 && !LIFT), "half k-stages: sparse 8-bit kinds");
+  static constexpr int A_ROW = KH ? 64 : 128;                // A bytes per row per stage
+  static constexpr uint32_t A_LAYOUT = KH ? 4u : 2u;         // UMMA desc: SWIZZLE_64B / SWIZZLE_128B
   static constexpr int A_SUB = 128 * A_ROW;                  // one swizzle-atom column of 128 rows
   static constexpr int A_STAGE = MSUB * A_SUB;
-  static constexpr int B_ATOMS = SPARSE ? 2 : 1;             // B bytes per stage = 2x A bytes for .sp
+  static constexpr int B_ATOMS = SPARSE && !KH ? 2 : 1;      // B bytes per stage = 2x A bytes for .sp
   static constexpr int B_ATOM = B_ROWS * 128;
   static constexpr int B_STAGE = B_ATOM * B_ATOMS;
   // 128x128b metadata atoms per stage and subtile: a stage is 128 bytes of
   // compressed A per row = 256 logical k for 8-bit kinds (2 atoms, 2 TMEM
   // columns per K=64 MMA) and 128 logical k for BF16 (1 atom, 1 column per
   // K=32 MMA); 1 metadata bit per logical k either way
-  static constexpr int E_ATOMS = KIND == MmaKind::F16 ? 1 : 2;
+  static constexpr int E_ATOMS = (KIND == MmaKind::F16 || KH) ? 1 : 2;
   static constexpr int E_PER_MMA = KIND == MmaKind::F16 ? 1 : 2;
   static constexpr int E_SUB = SPARSE ? E_ATOMS * 128 * 16 : 0;
   static constexpr int E_STAGE = MSUB * E_SUB;
   static constexpr int STAGE_TX = A_STAGE + B_STAGE + E_STAGE;
   static constexpr int K_BYTES_B = 128 * B_ATOMS;            // activation bytes consumed per stage
-  static constexpr int MMAS = 4;                             // k-steps per stage
+  static constexpr int MMAS = KH ? 2 : 4;                    // k-steps per stage
   static constexpr int ACC_COLS = BN;                        // 32-bit TMEM columns per accumulator
   static constexpr int E_COL = ACC_STAGES * MSUB * BN;       // metadata columns after the accumulators
   static constexpr int TMEM_COLS = 512;
@@ -112,7 +118,7 @@ struct Cfg {
   static constexpr int OUT_ESZ = OUT == SLSP_OUT_RAW_NM ? 4 : 2;
   // MSUB=1: 128-byte staging rows (64 BF16 / 32 int32 columns), so every TMA
   // store writes whole 128-byte lines (measured: L2 write cost is per request)
-  static constexpr int EPI_COLS = EW_ ? EW_ : epi_cols(MSUB, BN, OUT);
+  static constexpr int EPI_COLS = epi_cols(MSUB, BN, OUT);
   // (LIFT with two subtiles: one staging buffer, so the ring keeps 3 stages)
   static constexpr int EPI_BUFS = LIFT && MSUB == 2 ? 1 : 2;
   static constexpr int EPI_BUF = 32 * EPI_COLS * OUT_ESZ;
@@ -548,7 +554,8 @@ __global__ void __launch_bounds__(C::THREADS, 1)
           if (no_mma) return;
           const uint32_t a_base = smem_u32(sA + st * C::A_STAGE + h * C::A_SUB);
           const uint32_t b_base = smem_u32(sB + st * C::B_STAGE);
-          const uint32_t e_col = C::E_COL + 8 * h;
+          // KH: alternate halves of the subtile's 8 metadata columns between stages
+          const uint32_t e_col = C::E_COL + 8 * h + (C::KH ? 4 * (kb & 1) : 0);
           if constexpr (C::SPARSE) {
             const uint32_t e_base = smem_u32(sE + st * C::E_STAGE + h * C::E_SUB);
 #pragma unroll
@@ -1094,13 +1101,13 @@ int run(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const 
   return SLSP_OK;
 }
 
-template <bool SPARSE, MmaKind K, int BN, int MSUB, int LIFT, int EW>
+template <bool SPARSE, MmaKind K, int BN, int MSUB, int LIFT, int KH>
 int run_out_cl(int out_mode, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const CUtensorMap& o,
                const Params& p, cudaStream_t s) {
   switch (out_mode) {  // STAGES = 0: as many as fit
-    case SLSP_OUT_RAW_NM: return run<Cfg<SPARSE, K, BN, 0, SLSP_OUT_RAW_NM, MSUB, LIFT, EW>>(a, b, e, o, p, s);
-    case SLSP_OUT_BF16_NM: return run<Cfg<SPARSE, K, BN, 0, SLSP_OUT_BF16_NM, MSUB, LIFT, EW>>(a, b, e, o, p, s);
-    case SLSP_OUT_BF16_MN: return run<Cfg<SPARSE, K, BN, 0, SLSP_OUT_BF16_MN, MSUB, LIFT, EW>>(a, b, e, o, p, s);
+    case SLSP_OUT_RAW_NM: return run<Cfg<SPARSE, K, BN, 0, SLSP_OUT_RAW_NM, MSUB, LIFT, KH>>(a, b, e, o, p, s);
+    case SLSP_OUT_BF16_NM: return run<Cfg<SPARSE, K, BN, 0, SLSP_OUT_BF16_NM, MSUB, LIFT, KH>>(a, b, e, o, p, s);
+    case SLSP_OUT_BF16_MN: return run<Cfg<SPARSE, K, BN, 0, SLSP_OUT_BF16_MN, MSUB, LIFT, KH>>(a, b, e, o, p, s);
   }
   return SLSP_ERR_INVALID;
 }
@@ -1109,7 +1116,10 @@ int run_out_cl(int out_mode, const CUtensorMap& a, const CUtensorMap& b, const C
 // sparse kernel, SLSP_DGEMM_MSUB for the dense one; decode tiles: 1).
 template <bool SPARSE, MmaKind K, int BN, int LIFT = 0>
 int run_out(int out_mode, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const CUtensorMap& o,
-            const Params& p, cudaStream_t s, uint32_t msub) {
+            const Params& p, cudaStream_t s, uint32_t msub, uint32_t kh = 0) {
+  if constexpr (BN >= 128 && SPARSE && !LIFT && K != MmaKind::F16)
+    if (msub == 2 && kh && out_mode == SLSP_OUT_BF16_NM)
+      return run_out_cl<SPARSE, K, BN, 2, 0, 1>(out_mode, a, b, e, o, p, s);
   if constexpr (BN >= 128)
     if (msub == 2) return run_out_cl<SPARSE, K, BN, 2, LIFT, 0>(out_mode, a, b, e, o, p, s);
   return run_out_cl<SPARSE, K, BN, 1, LIFT, 0>(out_mode, a, b, e, o, p, s);
@@ -1120,6 +1130,7 @@ constexpr int kDenseBN = 256;
 // Decode-shaped M (<= 64 tokens): 64-token tiles, so the smem ring holds
 // mostly weight bytes (8 stages instead of 4) for the HBM-bound weight stream.
 constexpr int kDecodeBN = 64;
+constexpr uint32_t kSparseKHalf = 0;  // env SLSP_GEMM_KHALF
 constexpr int64_t kDecodeM = 64;
 constexpr uint32_t kDenseMsub = 1;
 constexpr uint32_t kRasterGroup = 16;  // measured best of {4, 8, 16, 32, 148} on Qwen2.5-7B shapes
@@ -1168,22 +1179,28 @@ int sparse_entry(int dtype, const void* values, const uint8_t* meta, int64_t n, 
   const int esz = dtype == SLSP_DT_BF16 ? 2 : 1;
   CUtensorMap ta, tb, te, to;
   Params p{};
-  if ((st = make_map_2d(&ta, values, kp / 2 * esz, n, 128))) return st;
+
   const bool decode = !LIFT && m <= kDecodeM;
   const int bn = decode ? kDecodeBN : kSparseBN;
   const uint32_t msub = decode ? 1u : env_knob("SLSP_GEMM_MSUB", sparse_msub(n, m)) == 2 ? 2u : 1u;
+  // half k-stages: the two-subtile BF16 [N][M] config of the 8-bit kinds
+  const uint32_t kh = (!LIFT && !decode && msub == 2 && esz == 1 && out_mode == SLSP_OUT_BF16_NM &&
+                       env_knob("SLSP_GEMM_KHALF", kSparseKHalf))
+                          ? 1u
+                          : 0u;
   if (ws && ws_bytes >= 2 * n * m * 4) {  // split-K partial-sum slices
     p.ws = ws;
     p.ws_cap = ws_bytes;
   }
   if ((st = make_map_2d(&tb, act, act_row * esz, m, bn / 2))) return st;
-  // BF16: a 128-byte A stage is 128 logical k -> one 2 KB metadata atom per stage
-  if ((st = make_map_meta(&te, meta, n, kp, esz == 2 ? 8 : 16))) return st;
+  if ((st = make_map_2d(&ta, values, kp / 2 * esz, n, 128, kh ? 64 : 128))) return st;
+  // BF16 and half k-stages: a stage is 128 logical k -> one 2 KB metadata atom
+  if ((st = make_map_meta(&te, meta, n, kp, (esz == 2 || kh) ? 8 : 16))) return st;
   if ((st = make_map_out(&to, out, out_mode, n, m, ldo, epi_cols(msub, bn, out_mode), &p.tma_store))) return st;
   select_epilogue(p, out_mode, msub, out, ldo, s_tok);
   p.n = n;
   p.m = m;
-  p.num_kb = static_cast<int>(kp * esz / 256);
+  p.num_kb = static_cast<int>(kp * esz / (kh ? 128 : 256));
   p.s_ch = s_ch;
   p.s_tok = s_tok;
   p.out = out;
@@ -1201,8 +1218,8 @@ int sparse_entry(int dtype, const void* values, const uint8_t* meta, int64_t n, 
     }
     if (dtype == SLSP_DT_BF16) return run_out<true, MmaKind::F16, kSparseBN>(out_mode, ta, tb, te, to, p, s, msub);
   }
-  if (dtype == SLSP_DT_I8) return run_out<true, MmaKind::I8, kSparseBN, L>(out_mode, ta, tb, te, to, p, s, msub);
-  return run_out<true, MmaKind::F8, kSparseBN, L>(out_mode, ta, tb, te, to, p, s, msub);
+  if (dtype == SLSP_DT_I8) return run_out<true, MmaKind::I8, kSparseBN, L>(out_mode, ta, tb, te, to, p, s, msub, kh);
+  return run_out<true, MmaKind::F8, kSparseBN, L>(out_mode, ta, tb, te, to, p, s, msub, kh);
 }
 
 }  // namespace

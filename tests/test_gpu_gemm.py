@@ -237,3 +237,38 @@ def test_gpu_check_equivalence_rejects_noncompliant(slsp):
     x = torch.ones((64, 32), dtype=torch.int8, device="cuda")
     with pytest.raises(slsp.NotCompliantError, match="row 0, block 0"):
         slsp.check_equivalence(w, x, 6, 8)
+
+
+@pytest.mark.parametrize("kind", ["int8", "fp8"])
+def test_half_k_stage_config_identical(slsp, kind):
+    """The half-k-stage tile config (SLSP_GEMM_KHALF: 64-byte A rows, one
+    metadata atom and two MMAs per stage) reproduces the default config's
+    BF16 output bit for bit (INT8: same exact sums; FP8: same MMA order)."""
+    import os
+
+    g = torch.Generator(device="cuda").manual_seed(11)
+    n, k, m = 1536, 3584, 1000
+    if kind == "int8":
+        w = slsp.magnitude_prune(torch.randint(-127, 128, (n, k), dtype=torch.int8, device="cuda", generator=g), 6, 8)
+        qk = slsp.QUANT_INT8
+    else:
+        w = slsp.magnitude_prune(((torch.rand(n, k, device="cuda", generator=g) * 2 - 1) * 200).to(torch.float8_e4m3fn),
+                                 6, 8)
+        qk = slsp.QUANT_FP8E4M3
+    x = (torch.rand(m, k, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    s_ch = torch.rand(n, device="cuda", generator=g) * 0.01 + 0.001
+    pw = slsp.pack_compress(w, 6, 8)
+    payload, s_tok = slsp.fused_quant_slide(x, 6, 8, kind=qk)
+    outs = []
+    for kh in ("0", "1"):
+        os.environ["SLSP_GEMM_KHALF"] = kh
+        try:
+            outs.append(slsp.sparse_gemm(pw, payload, s_ch=s_ch, s_tok=s_tok, out_mode=slsp.OUT_BF16_NM))
+        finally:
+            del os.environ["SLSP_GEMM_KHALF"]
+    torch.cuda.synchronize()
+    if kind == "int8":
+        assert torch.equal(outs[0].view(torch.int16), outs[1].view(torch.int16))
+    else:  # fp32 accumulation: the per-MMA k order is the same, so equal in practice; allow 1 bf16 ulp
+        diff = (outs[0].float() - outs[1].float()).abs()
+        assert torch.all(diff <= outs[0].float().abs() * 2 ** -7 + 1e-6)
