@@ -379,6 +379,14 @@ SLSP_DEVINL void tmem_ld_wait_regs(uint32_t (&r)[16]) {
                : "memory");
 }
 
+// Programmatic dependent launch (sm_90+): a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may start its prologue
+// while the previous kernel in the stream drains; pdl_wait() blocks until that
+// kernel has completed and its memory is visible, pdl_trigger() lets the next
+// kernel launch. Both are no-ops for kernels launched without the attribute.
+SLSP_DEVINL void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+SLSP_DEVINL void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 SLSP_DEVINL uint4 ld_shared_u4(uint32_t addr) {
   uint4 v;
   asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));

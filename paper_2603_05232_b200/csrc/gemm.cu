@@ -444,6 +444,10 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // PDL: the prologue above overlapped the previous kernel's tail; from here
+  // on every role touches memory that kernel may have produced or read
+  pdl_wait();
+  pdl_trigger();
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer ----
@@ -1055,16 +1059,18 @@ int run(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const 
   static int max_clusters = 0;
   auto kern = gemm_kernel<C>;
   cudaLaunchConfig_t cfg{};
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = C::CL;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = slsp_host::pdl_enabled() ? 1 : 0;
   cfg.blockDim = dim3(C::THREADS);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = s;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   if (!max_clusters) {  // how many clusters of this shape are co-resident (GPC packing)
     SLSP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     cfg.gridDim = dim3(C::CL * (num_sms() / C::CL));

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "../../include/slsp_b200.h"
 
 namespace slsp_host {
@@ -33,6 +35,27 @@ int status_collect(void* status_ws, cudaStream_t s, int err_code, int64_t* row, 
 
 // Current device must be sm_100 (B200); fails loudly otherwise.
 int require_sm100();
+
+// Programmatic dependent launch for the hot kernels (env SLSP_PDL=1 turns it on).
+bool pdl_enabled();
+
+// cudaLaunchKernelEx with the programmatic-stream-serialization attribute
+// (PDL) when enabled; plain launch semantics otherwise.
+template <typename... KArgs, typename... Args>
+int launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  SLSP_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+  return SLSP_OK;
+}
 
 inline int elem_size(int dtype) {
   switch (dtype) {

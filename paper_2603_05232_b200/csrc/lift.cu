@@ -496,6 +496,8 @@ __global__ void __launch_bounds__(1024) act_row1_kernel(ActArgs a) {  // one row
   __shared__ float s_max[32];
   const int nquads = static_cast<int>(a.cols / G::ELEMS);
   uint4 v[QPT][G::IN_VEC];
+  pdl_wait();  // the activations may come from the previous kernel (PDL launch)
+  pdl_trigger();
   row_load<IN, KIND, L, QPT>(a, blockIdx.x, nquads, v);
   row_emit<IN, KIND, L, QPT>(a, blockIdx.x, nquads, s_max, v);
 }
@@ -503,9 +505,8 @@ __global__ void __launch_bounds__(1024) act_row1_kernel(ActArgs a) {  // one row
 template <int IN, int KIND, int L, int QPT>
 int launch_row_q(ActArgs& a, int threads, cudaStream_t s) {
   if (a.rows >= (int64_t{1} << 31)) return SLSP_ERR_UNSUPPORTED;
-  act_row1_kernel<IN, KIND, L, QPT><<<static_cast<unsigned>(a.rows), threads, 0, s>>>(a);
-  SLSP_LAUNCH_CHECK();
-  return SLSP_OK;
+  return slsp_host::launch_pdl(act_row1_kernel<IN, KIND, L, QPT>, dim3(static_cast<unsigned>(a.rows)), dim3(threads),
+                               0, s, a);
 }
 
 // Row-resident launch when the row fits (<= 4 quads per thread, <= 1024

@@ -1,5 +1,6 @@
 // C-ABI plumbing: versioning, status scratch, plan geometry, device checks.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "internal.h"
@@ -44,6 +45,14 @@ int require_sm100() {
     return SLSP_ERR_CUDA;
   }
   return SLSP_OK;
+}
+
+bool pdl_enabled() {  // off by default: measured 1% slower on the bench step
+  static const bool on = [] {
+    const char* e = std::getenv("SLSP_PDL");
+    return e && e[0] == '1';
+  }();
+  return on;
 }
 
 }  // namespace slsp_host
