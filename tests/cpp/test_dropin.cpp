@@ -4,7 +4,9 @@
 // executed on the GPU through libslsp_b200.so. Exit code = number of failures.
 // Built by tests/cpp/Makefile; run by tests/test_gpu_dropin.py.
 #include <cstdio>
+#include <fstream>
 #include <functional>
+#include <iterator>
 #include <limits>
 #include <random>
 #include <string>
@@ -141,6 +143,37 @@ int main() {
     CHECK(verify_compliance(s, 2, 4).compliant);
     CHECK(unslide(s).data == pruned.data);
     CHECK(decompress(compress(s)).data == s.data);
+  }
+  // container.hpp: files the REFERENCE wrote (tests/golden, gen_golden.py) —
+  // parse, typed conversion, byte-exact re-serialization, the GEMM on the
+  // loaded weights == the GEMM on weights packed here (test_container.cpp)
+  {
+    const std::string gold = std::string(SLSP_GOLDEN_DIR) + "/";
+    for (const char* tag : {"even", "odd"}) {
+      const auto path = gold + "container_6_8_" + tag + ".slsp";
+      const auto c = load_container(path);
+      CHECK(c.kind == Kind::compressed && c.z == 6 && c.l == 8);
+      const auto cm = compressed_from<std::int8_t>(c);
+      std::ifstream f(path, std::ios::binary);
+      const std::vector<std::uint8_t> bytes((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+      CHECK(serialize(to_container(cm)) == bytes);
+      // the same weights through this library's packer give the same operands
+      const auto w = unslide(decompress(cm));
+      const auto mine = compress(pack_matrix(w, SparsityPattern(6, 8)));
+      CHECK(mine.values == cm.values && mine.metadata == cm.metadata);
+      std::mt19937_64 rng(5);
+      Matrix<float> x(7, w.cols);
+      std::uniform_real_distribution<float> dx(-1.0f, 1.0f);
+      for (auto& v : x.data) v = dx(rng);
+      const auto act = fused_quant_slide(x, SparsityPattern(6, 8), QuantKind::int8);
+      CHECK(sparse_gemm(cm, act).data == sparse_gemm(mine, act).data);
+    }
+    const auto q = quantized_from(load_container(gold + "container_fqs_6_8.slsp"));
+    CHECK(q.rows == 9 && q.words_per_row * 4 == 144 && q.kind == QuantKind::int8);
+    auto bad = serialize(to_container(q));
+    bad[40] ^= 0x5A;
+    CHECK(throws<ContainerError>([&] { deserialize(bad); }));
+    CHECK(throws<ContainerError>([&] { deserialize(std::vector<std::uint8_t>(10, 0)); }));
   }
   std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "OK", failures);
   return failures;
