@@ -108,7 +108,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:  # noqa: BLE001
                 pass
-            time.sleep(0.02)
+            time.sleep(0.004)
 
     def __enter__(self):
         if self.nvml:

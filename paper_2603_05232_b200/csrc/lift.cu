@@ -490,8 +490,10 @@ SLSP_DEVINL void row_emit(const ActArgs& a, int64_t row, int nquads, float* s_ma
   for (int i = nquads * G::OUT_VEC + tid; i < out_vecs; i += nthr) dst[i] = make_uint4(0, 0, 0, 0);  // kp padding
 }
 
-template <int IN, int KIND, int L, int QPT>
-__global__ void __launch_bounds__(1024) act_row1_kernel(ActArgs a) {  // one row per CTA, grid = rows
+// MAXT/MINB: launch bounds; the <=128-thread instantiation asks for 16
+// resident CTAs (<= 32 registers) so more rows are in flight per SM.
+template <int IN, int KIND, int L, int QPT, int MAXT = 1024, int MINB = 1>
+__global__ void __launch_bounds__(MAXT, MINB) act_row1_kernel(ActArgs a) {  // one row per CTA, grid = rows
   using G = WarpGeom<IN, KIND, L>;
   __shared__ float s_max[32];
   const int nquads = static_cast<int>(a.cols / G::ELEMS);
@@ -505,6 +507,9 @@ __global__ void __launch_bounds__(1024) act_row1_kernel(ActArgs a) {  // one row
 template <int IN, int KIND, int L, int QPT>
 int launch_row_q(ActArgs& a, int threads, cudaStream_t s) {
   if (a.rows >= (int64_t{1} << 31)) return SLSP_ERR_UNSUPPORTED;
+  if (threads <= 128 && env_row_path() != 2)
+    return slsp_host::launch_pdl(act_row1_kernel<IN, KIND, L, QPT, 128, 16>, dim3(static_cast<unsigned>(a.rows)),
+                                 dim3(threads), 0, s, a);
   return slsp_host::launch_pdl(act_row1_kernel<IN, KIND, L, QPT>, dim3(static_cast<unsigned>(a.rows)), dim3(threads),
                                0, s, a);
 }
