@@ -1152,6 +1152,7 @@ uint32_t sparse_msub(int64_t n, int64_t m) {
 
 
 int check_out(int out_mode, const float* s_ch, const float* s_tok, void* out, int64_t ldo, int64_t n, int64_t m) {
+  if (n == 0 || m == 0) return SLSP_OK;  // empty result (the reference returns an empty matrix)
   if (!out) return SLSP_ERR_INVALID;
   if (out_mode == SLSP_OUT_RAW_NM || out_mode == SLSP_OUT_BF16_NM) {
     if (ldo < m) return SLSP_ERR_INVALID;

@@ -611,6 +611,7 @@ int slsp_gemm_order(int dtype, const void* values, const uint8_t* codes, int64_t
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int esz = elem_size(dtype);
   if ((esz != 1 && esz != 2) || rows < 0 || cols <= 0 || kp_ref <= 0 || kp_ref % 4 != 0) return SLSP_ERR_INVALID;
+  if (rows == 0) return SLSP_OK;
   if (!values || !codes || !values_out || !codes_out) return SLSP_ERR_INVALID;
   const int64_t nblk = (cols + 7) / 8;
   if (kp_ref < nblk * 12) return SLSP_ERR_DIMENSION;  // the reference width must hold every real window
@@ -634,8 +635,9 @@ int slsp_load_compressed(int dtype, const void* values, const uint8_t* codes_str
   using namespace slsp_host;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int esz = elem_size(dtype);
-  if ((esz != 1 && esz != 2) || rows < 0 || windows < 0 || !values || !codes_stream || !values_out || !meta_out)
-    return SLSP_ERR_INVALID;
+  if ((esz != 1 && esz != 2) || rows < 0 || windows < 0) return SLSP_ERR_INVALID;
+  if (rows == 0) return SLSP_OK;
+  if (!values || !codes_stream || !values_out || !meta_out) return SLSP_ERR_INVALID;
   if (kp % 8 != 0 || kp / 4 < windows) return SLSP_ERR_DIMENSION;
   int st;
   if ((st = require_sm100())) return st;
@@ -658,8 +660,10 @@ int slsp_tile_meta(const uint8_t* meta, int64_t rows, int64_t kp, uint8_t* tiled
 int slsp_tile_meta_ex(const uint8_t* meta, int64_t rows, int64_t kp, int dtype, uint8_t* tiled, slsp_stream_t stream) {
   using namespace slsp_host;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (rows < 0 || kp <= 0 || !meta || !tiled) return SLSP_ERR_INVALID;
+  if (rows < 0 || kp <= 0) return SLSP_ERR_INVALID;
   if (kp % 256 != 0) return SLSP_ERR_DIMENSION;
+  if (rows == 0) return SLSP_OK;
+  if (!meta || !tiled) return SLSP_ERR_INVALID;
   if ((reinterpret_cast<uintptr_t>(meta) | reinterpret_cast<uintptr_t>(tiled)) & 15u) return SLSP_ERR_INVALID;
   int st;
   if ((st = require_sm100())) return st;

@@ -272,3 +272,23 @@ def test_half_k_stage_config_identical(slsp, kind):
     else:  # fp32 accumulation: the per-MMA k order is the same, so equal in practice; allow 1 bf16 ulp
         diff = (outs[0].float() - outs[1].float()).abs()
         assert torch.all(diff <= outs[0].float().abs() * 2 ** -7 + 1e-6)
+
+
+def test_empty_inputs(slsp):
+    """Empty shapes behave like the reference's (empty results, no error):
+    zero tokens, zero weight rows."""
+    g = torch.Generator(device="cuda").manual_seed(3)
+    w = slsp.magnitude_prune(torch.randint(-127, 128, (256, 512), dtype=torch.int8, device="cuda", generator=g), 6, 8)
+    pw = slsp.pack_compress(w, 6, 8)
+    x0 = torch.empty((0, 512), dtype=torch.bfloat16, device="cuda")
+    payload, s_tok = slsp.fused_quant_slide(x0, 6, 8)
+    assert payload.shape == (0, pw.kp // 4) and s_tok.numel() == 0
+    y = slsp.sparse_gemm(pw, payload)
+    assert y.shape == (256, 0)
+    q, qs = slsp.quantize_rows(x0)
+    assert slsp.dense_gemm(w, q.view(torch.int8)).shape == (256, 0)
+    w0 = torch.empty((0, 512), dtype=torch.int8, device="cuda")
+    pw0 = slsp.pack_compress(w0, 6, 8)
+    x = (torch.rand(64, 512, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    payload, s_tok = slsp.fused_quant_slide(x, 6, 8)
+    assert slsp.sparse_gemm(pw0, payload).shape == (0, 64)
