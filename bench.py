@@ -291,6 +291,24 @@ def run_b200(args, world, rank, local):
             torch.cuda.synchronize()
             allgather = {"ms_per_step": reduce_max(ev0.elapsed_time(ev1)),
                          "bytes_per_rank": sum(2 * m * L.n_total for L in layers)}
+        else:  # [N][M] shards are contiguous row blocks: one all_gather_into_tensor per layer
+            from paper_2603_05232_b200.sharding import shard_size
+
+            per = [shard_size(L.n_total, world) for L in layers]
+            send = [torch.zeros((p_, m), dtype=torch.bfloat16, device=device) for p_ in per]
+            recv = [torch.empty((p_ * world, m), dtype=torch.bfloat16, device=device) for p_ in per]
+            for i, L in enumerate(layers):
+                send[i][: L.n].copy_(outs[i])
+            for _ in range(2):
+                ev0.record(stream)
+                for i in range(len(layers)):
+                    dist.all_gather_into_tensor(recv[i], send[i])
+                ev1.record(stream)
+            torch.cuda.synchronize()
+            allgather = {"ms_per_step": reduce_max(ev0.elapsed_time(ev1)),
+                         "bytes_per_rank": sum(2 * m * p_ * world for p_ in per),
+                         "what": "NCCL all_gather_into_tensor of the [N/world][M] BF16 output shards (padded to "
+                                 "128-row blocks), timed alone after the GEMM step"}
 
     # ---- roofline of the dominant kernel (the sparse GEMM) ----
     peaks = json.loads(PEAKS_FILE.read_text()) if PEAKS_FILE.exists() else {}
