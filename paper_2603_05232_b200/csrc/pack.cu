@@ -5,6 +5,8 @@
 // ("group"); the greedy placement depends only on the block's l-bit nonzero
 // mask, so it runs in registers on bit masks. Outputs are staged in shared
 // memory per 256-group chunk and written back with 32-bit coalesced stores.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -347,6 +349,97 @@ __global__ void __launch_bounds__(256) pack68_kernel(const uint8_t* __restrict__
   }
 }
 
+// 8-bit weights, byte-permute form of the same table: per mask, PRMT
+// selectors placing the window values (output bytes 0-3 and 4-5 of a block)
+// from the block's 8 bytes, a keep-mask that zeroes the padding slots (a -0
+// e4m3 byte is "zero" to the packer but not the 0x00 padding value, so the
+// padding is masked, not selected), and the 12 code bits. ~2.5 instructions
+// per weight byte instead of ~6 (the table-walk form was issue-bound: 64%
+// issue-active, math-pipe throttle, ncu profiles/r01_ncu_full.txt).
+struct Lut8p {
+  unsigned long long sel[256];   // bits 0-15 bytes 0-3, 16-23 bytes 4-5, 32-43 codes
+  unsigned long long keep[256];  // bytes 0-3 mask (bits 0-31), bytes 4-5 mask (bits 32-47)
+};
+
+Lut8p build_lut8p(const Lut8& t) {
+  Lut8p p{};
+  for (int mask = 0; mask < 256; ++mask) {
+    unsigned long long sel = 0, keep = 0, codes = 0;
+    for (int w = 0; w < 3; ++w) {
+      const uint32_t f = static_cast<uint32_t>(t.e[mask] >> (16 * w));
+      codes |= static_cast<unsigned long long>(f & 0xFu) << (4 * w);
+      for (int sl = 0; sl < 2; ++sl) {
+        const int ob = 2 * w + sl;  // output byte 0..5 of the block
+        const uint32_t so = (f >> (4 + 4 * sl)) & 0xFu;
+        const unsigned long long nib = so < 8 ? so : 0;  // any byte; masked below
+        const int shift = ob < 4 ? 4 * ob : 16 + 4 * (ob - 4);
+        sel |= nib << shift;
+        if (so < 8) keep |= 0xFFull << (ob < 4 ? 8 * ob : 32 + 8 * (ob - 4));
+      }
+    }
+    p.sel[mask] = sel | (codes << 32);
+    p.keep[mask] = keep;
+  }
+  return p;
+}
+
+__global__ void __launch_bounds__(256) pack68b_kernel(const uint8_t* __restrict__ w, int64_t rows, int64_t cols, int z,
+                                                      int dtype, const Lut8p* __restrict__ lut, uint8_t* __restrict__ values,
+                                                      int64_t ld_vals, uint8_t* __restrict__ meta, int64_t ld_meta,
+                                                      unsigned long long* status) {
+  __shared__ unsigned long long s_sel[256], s_keep[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    s_sel[i] = lut->sel[i];
+    s_keep[i] = lut->keep[i];
+  }
+  __syncthreads();
+  const int64_t octs = cols / 64;  // 8 blocks of 8 per thread
+  const int64_t total = rows * octs;
+  const unsigned long long m7 = 0x7F7F7F7F7F7F7F7Full;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t row = idx / octs, q = idx - row * octs;
+    const uint4* src = reinterpret_cast<const uint4*>(w + row * cols + q * 64);
+    uint4 v[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = __ldg(src + i);
+    const uint32_t* x = reinterpret_cast<const uint32_t*>(v);  // block g = words 2g, 2g+1
+    uint32_t ov[12];
+    uint32_t om[3] = {0, 0, 0};
+#pragma unroll
+    for (int g = 0; g < 8; g += 2) {
+      uint32_t P[2], Q[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t lo = x[2 * (g + h)], hi = x[2 * (g + h) + 1];
+        const unsigned long long b64 = (static_cast<unsigned long long>(hi) << 32) | lo;
+        const unsigned long long b = dtype == SLSP_DT_E4M3 ? (b64 & m7) : b64;
+        const unsigned long long t = (((b & m7) + m7) | b) & 0x8080808080808080ull;
+        const uint32_t mask = static_cast<uint32_t>(((t >> 7) * 0x0102040810204080ull) >> 56);
+        if (__popc(mask) > z) record_error(status, row, q * 8 + g + h);  // first_overfull_block
+        const unsigned long long sel = s_sel[mask], keep = s_keep[mask];
+        P[h] = __byte_perm(lo, hi, static_cast<uint32_t>(sel) & 0xFFFFu) & static_cast<uint32_t>(keep);
+        Q[h] = __byte_perm(lo, hi, static_cast<uint32_t>(sel >> 16) & 0xFFu) & static_cast<uint32_t>(keep >> 32);
+        const uint32_t c = static_cast<uint32_t>(sel >> 32) & 0xFFFu;  // 12 code bits of block g+h
+        const int bit = 12 * (g + h);
+        om[bit >> 5] |= c << (bit & 31);
+        if ((bit & 31) > 20) om[(bit >> 5) + 1] |= c >> (32 - (bit & 31));
+      }
+      // blocks A, B (6 bytes each) -> 3 words: [A0-3] [A4 A5 B0 B1] [B2-5]
+      ov[3 * (g >> 1)] = P[0];
+      ov[3 * (g >> 1) + 1] = __byte_perm(Q[0], P[1], 0x5410);
+      ov[3 * (g >> 1) + 2] = __byte_perm(P[1], Q[1], 0x5432);
+    }
+    uint4* dv = reinterpret_cast<uint4*>(values + row * ld_vals + q * 48);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) dv[i] = make_uint4(ov[4 * i], ov[4 * i + 1], ov[4 * i + 2], ov[4 * i + 3]);
+    uint32_t* dm = reinterpret_cast<uint32_t*>(meta + row * ld_meta + q * 12);
+    dm[0] = om[0];
+    dm[1] = om[1];
+    dm[2] = om[2];
+  }
+}
+
 // Row-major 2-bit codes -> MMA-tiled metadata (see slsp_tile_meta in the
 // header): one 16-byte chunk per thread, coalesced on the tiled side.
 // F16 (16-bit A, kind::f16) variant: the 2 KB metadata atom of 128 rows x
@@ -474,6 +567,22 @@ __global__ void load_compressed_kernel(const uint8_t* __restrict__ vals, const u
   }
 }
 
+// The byte-permute table lives in device memory (4 KB, uploaded once per
+// process; too large for a kernel parameter). Env SLSP_PACK_PATH=1 selects the
+// table-walk kernel (perf probing).
+const Lut8p* upload_lut8p(const Lut8& t) {
+  static Lut8p host = build_lut8p(t);
+  void* d = nullptr;
+  if (cudaMalloc(&d, sizeof(Lut8p)) != cudaSuccess) return nullptr;
+  if (cudaMemcpy(d, &host, sizeof(Lut8p), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+  return static_cast<const Lut8p*>(d);
+}
+
+int pack_path() {
+  const char* e = std::getenv("SLSP_PACK_PATH");
+  return e && *e ? e[0] - '0' : 2;
+}
+
 template <int MODE>
 int launch_pack(int esz, PackArgs& a, cudaStream_t s) {
   const int64_t chunks = (a.group_slots + kThreads - 1) / kThreads;
@@ -572,7 +681,13 @@ int slsp_pack_compress(int dtype, const void* w, int64_t rows, int64_t cols, int
       const auto* in = static_cast<const uint8_t*>(w);
       auto* out = static_cast<uint8_t*>(values);
       if (esz == 1)
-        pack68_kernel<1><<<grid, 256, 0, s>>>(in, rows, cols, z, dtype, lut, out, ld_vals, meta, ld_meta, status);
+        if (pack_path() == 1) {
+          pack68_kernel<1><<<grid, 256, 0, s>>>(in, rows, cols, z, dtype, lut, out, ld_vals, meta, ld_meta, status);
+        } else {
+          static const Lut8p* dlut = upload_lut8p(lut);
+          if (!dlut) return SLSP_ERR_CUDA;
+          pack68b_kernel<<<grid, 256, 0, s>>>(in, rows, cols, z, dtype, dlut, out, ld_vals, meta, ld_meta, status);
+        }
       else
         pack68_kernel<2><<<grid, 256, 0, s>>>(in, rows, cols, z, dtype, lut, out, ld_vals, meta, ld_meta, status);
       SLSP_LAUNCH_CHECK();
