@@ -15,9 +15,14 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
    python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu > $out/ncu_launch.log 2>&1; echo "ncu launches exit $?"
 # full captures (3rd launch of each: warm): sparse gate_up GEMM, dense gate_up GEMM, lift (K=3584), 6:8 packer
 NCU="ncu --set full --clock-control none --import-source on"
-timeout 600 $NCU -k regex:gemm_kernel -s 2 -c 1 -o $out/prof_sgemm python tests/probes/probe_one.py sparse gate_up > $out/ncu_s.log 2>&1
-timeout 600 $NCU -k regex:gemm_kernel -s 2 -c 1 -o $out/prof_dgemm python tests/probes/probe_one.py dense gate_up > $out/ncu_d.log 2>&1
-timeout 600 $NCU -k regex:act_row1_kernel -s 2 -c 1 -o $out/prof_lift python tests/probes/probe_lift.py 3584 > $out/ncu_l.log 2>&1
-timeout 600 $NCU -k regex:pack68_kernel -s 0 -c 1 -o $out/prof_pack python tests/probes/probe_pack.py > $out/ncu_p.log 2>&1
+timeout 600 $NCU -k regex:gemm_kernel -s 2 -c 1 -o /tmp/prof_sgemm python tests/probes/probe_one.py sparse gate_up > $out/ncu_s.log 2>&1
+timeout 600 $NCU -k regex:gemm_kernel -s 2 -c 1 -o /tmp/prof_dgemm python tests/probes/probe_one.py dense gate_up > $out/ncu_d.log 2>&1
+timeout 600 $NCU -k regex:act_row1_kernel -s 2 -c 1 -o /tmp/prof_lift python tests/probes/probe_lift.py 3584 > $out/ncu_l.log 2>&1
+timeout 600 $NCU -k regex:pack68b_kernel -s 0 -c 1 -o /tmp/prof_pack python tests/probes/probe_pack.py > $out/ncu_p.log 2>&1
+# the reports stay on the box (gpurun_out/ is capped at 64 MiB); bring back the summaries
+python tests/ncu_summary.py /tmp/prof_sgemm.ncu-rep /tmp/prof_dgemm.ncu-rep /tmp/prof_lift.ncu-rep /tmp/prof_pack.ncu-rep \
+   > $out/ncu_full.txt 2>&1
+python tests/ncu_summary.py --launches $out/launches.csv > $out/launches_summary.txt 2>&1
+for f in sgemm dgemm pack; do cp /tmp/prof_$f.ncu-rep $out/ 2>/dev/null; done
 ls -la $out/*.ncu-rep
 echo done
