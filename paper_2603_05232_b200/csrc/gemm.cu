@@ -142,7 +142,10 @@ struct Cfg {
   static constexpr int OFF_E = OFF_B + STAGES * B_STAGE;
   static constexpr int OFF_EPI = OFF_E + STAGES * E_STAGE;
   static constexpr int OFF_BAR = OFF_EPI + EPI_WARPS * EPI_WARP;
-  static constexpr int NUM_BARS = 3 * STAGES + 4;  // full, empty, xfull (LIFT) per stage; tfull, tempty
+  // Two-subtile stages signal subtile 1's operands (A1, E1) on a second
+  // barrier, so subtile 0's MMAs start once B, A0 and E0 have landed.
+  static constexpr bool SPLIT = MSUB == 2 && SPARSE && !LIFT;
+  static constexpr int NUM_BARS = 4 * STAGES + 4;  // full, empty, xfull, full1 per stage; tfull, tempty
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16 + 1024;  // + alignment slack
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
   static constexpr uint32_t C_FMT = KIND == MmaKind::I8 ? 2u : 1u;
@@ -171,6 +174,7 @@ struct Params {
   // fp32) into ws[s][n][m] and a finishing kernel sums the slices in order
   // (deterministic; exact for int32) and applies the epilogue. ksplit == 1:
   // the normal epilogue.
+  int splitbar;  // SPLIT configs: per-subtile full barriers (env SLSP_GEMM_SPLITBAR, default 1)
   int ksplit;
   void* ws;
   int64_t ws_cap;  // workspace bytes (bounds ksplit)
@@ -398,7 +402,8 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* empty = full + C::STAGES;
   uint64_t* xfull = empty + C::STAGES;  // LIFT: this CTA's X tile of a stage has landed
-  uint64_t* tfull = xfull + C::STAGES;
+  uint64_t* full1 = xfull + C::STAGES;  // SPLIT: subtile 1's A/E of a stage have landed
+  uint64_t* tfull = full1 + C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -426,6 +431,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       // MMA commit (+ LIFT: each local lift warp is done reading the stage's X tile)
       mbar_init(&empty[s], C::NPAIR + C::LIFT_WARPS);
       mbar_init(&xfull[s], 1);
+      mbar_init(&full1[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -483,18 +489,28 @@ __global__ void __launch_bounds__(C::THREADS, 1)
           if (no_load) {
             if (leader) mbar_arrive(&full[stage]);
             if (C::LIFT) mbar_arrive(&xfull[stage]);
+            if (C::SPLIT && leader) mbar_arrive(&full1[stage]);
           } else {
             const bool skip_e = p.debug & kDbgNoMeta;
             if (p.trace && blockIdx.x == 0 && it < 16 && kb < 256) p.trace[65536 + (it * 256 + kb) * 2] = clock64();
             const bool skip_b = !C::LIFT && (p.debug & kDbgSkipB3) && kb % 3 == 2;
-            if (leader)
-              mbar_arrive_expect_tx(&full[stage], 2 * (C::STAGE_TX - (skip_e ? C::E_STAGE : 0) -
-                                                       ((skip_b || C::LIFT) ? C::B_STAGE : 0)));
+            const bool split = C::SPLIT && p.splitbar;
+            const uint32_t tx_all = 2 * (C::STAGE_TX - (skip_e ? C::E_STAGE : 0) -
+                                         ((skip_b || C::LIFT) ? C::B_STAGE : 0));
+            const uint32_t tx1 = split ? 2 * (C::A_SUB + (skip_e ? 0 : C::E_SUB)) : 0;
+            if (leader) {
+              mbar_arrive_expect_tx(&full[stage], tx_all - tx1);
+              if constexpr (C::SPLIT) {
+                if (split) mbar_arrive_expect_tx(&full1[stage], tx1);
+                else mbar_arrive(&full1[stage]);
+              }
+            }
             const uint32_t bar = mapa_shared(smem_u32(&full[stage]), lead);
+            const uint32_t bar1 = split ? mapa_shared(smem_u32(&full1[stage]), lead) : bar;
 #pragma unroll
             for (int h = 0; h < C::MSUB; ++h)
-              tma_load_2d_cg2_hint(sA + stage * C::A_STAGE + h * C::A_SUB, &tmA, bar, kl * C::A_ROW, a_row + h * 256,
-                                   pol_a);
+              tma_load_2d_cg2_hint(sA + stage * C::A_STAGE + h * C::A_SUB, &tmA, h ? bar1 : bar, kl * C::A_ROW,
+                                   a_row + h * 256, pol_a);
             if constexpr (C::LIFT) {
               // X block j of period q: source bytes [512q + 256j, +256) into this CTA (local barrier)
               // xfull completes once per ring lap (slots alternate between X
@@ -520,7 +536,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
               if (!skip_e)
 #pragma unroll
                 for (int h = 0; h < C::MSUB; ++h)
-                  tma_load_2d_cg2_hint(sE + stage * C::E_STAGE + h * C::E_SUB, &tmE, bar, 0,
+                  tma_load_2d_cg2_hint(sE + stage * C::E_STAGE + h * C::E_SUB, &tmE, h ? bar1 : bar, 0,
                                        (((a_row + h * 256) >> 7) * p.num_kb + kl) * 8 * C::E_ATOMS, pol_a);
           }
           if (++stage == C::STAGES) {
@@ -588,6 +604,13 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         bool sub1_ready = C::MSUB == 1;
         long long wait_cycles = 0;
         int lag = 0, lag_stage = 0, lag_kb = 0;  // deferred subtile-1 k-blocks (consecutive ring stages)
+        uint32_t lag_phase = 0;
+        auto wait_full1 = [&](int st, uint32_t ph) {
+          if constexpr (C::SPLIT) {
+            mbar_wait(&full1[st], ph);
+            tc_fence_after();
+          }
+        };
         for (int kb = kb0; kb < kb1; ++kb) {
           if (p.trace) {
             const long long t0 = clock64();
@@ -603,12 +626,14 @@ __global__ void __launch_bounds__(C::THREADS, 1)
           if constexpr (C::MSUB == 1) {
             tc_commit_mc(&empty[stage], all_ctas);  // every CTA of the cluster
           } else if (sub1_ready) {
+            wait_full1(stage, phase);
             issue(1, stage, kb);
             tc_commit_mc(&empty[stage], all_ctas);
           } else {
             if (lag++ == 0) {
               lag_stage = stage;
               lag_kb = kb;
+              lag_phase = phase;
             }
             // catch up once subtile 1 is drained; block when the ring is
             // exhausted or the tile's k-loop ends
@@ -618,10 +643,15 @@ __global__ void __launch_bounds__(C::THREADS, 1)
               SLSP_TRACE(it, 1);
               sub1_ready = true;
               int st = lag_stage;
+              uint32_t ph = lag_phase;
               for (int i = 0; i < lag; ++i) {
+                wait_full1(st, ph);
                 issue(1, st, lag_kb + i);
                 tc_commit_mc(&empty[st], all_ctas);
-                if (++st == C::STAGES) st = 0;
+                if (++st == C::STAGES) {
+                  st = 0;
+                  ph ^= 1u;
+                }
               }
               lag = 0;
             }
@@ -1216,6 +1246,7 @@ int sparse_entry(int dtype, const void* values, const uint8_t* meta, int64_t n, 
   p.trace = reinterpret_cast<unsigned long long*>(env_ptr("SLSP_GEMM_TRACE"));
   p.hints = env_knob("SLSP_GEMM_HINTS", kDefaultHints);
   p.group = static_cast<int>(env_knob("SLSP_GEMM_GROUP", kRasterGroup));
+  p.splitbar = static_cast<int>(env_knob("SLSP_GEMM_SPLITBAR", 1));
   constexpr int L = LIFT ? 1 : 0;
   if constexpr (!LIFT) {
     if (decode) {
@@ -1300,6 +1331,7 @@ int slsp_dense_gemm_ws(int dtype, const void* w, int64_t n, int64_t k, const voi
   p.trace = reinterpret_cast<unsigned long long*>(env_ptr("SLSP_GEMM_TRACE"));
   p.hints = env_knob("SLSP_GEMM_HINTS", kDefaultHints);
   p.group = static_cast<int>(env_knob("SLSP_GEMM_GROUP", kRasterGroup));
+  p.splitbar = static_cast<int>(env_knob("SLSP_GEMM_SPLITBAR", 1));
   if (dtype == SLSP_DT_I8)
     return decode ? run_out<false, MmaKind::I8, kDecodeBN>(out_mode, ta, tb, ta, to, p, s, 1)
                   : run_out<false, MmaKind::I8, kDenseBN>(out_mode, ta, tb, ta, to, p, s, msub);
