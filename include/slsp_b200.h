@@ -204,7 +204,8 @@ SLSP_API int slsp_sparse_gemm_x(int dtype, const void* values, const uint8_t* me
                        slsp_stream_t stream);
 
 /* Workspace of the *_ws GEMM variants: 8*n*m*4 bytes for decode-shaped M
- * (m <= 256), else 0. With it, GEMMs whose tiles do not fill the 148 SMs
+ * (m <= 256), the same capped at 64 MiB (0 if that holds < 2 slices) for
+ * 256 < m <= 1024, else 0. With it, GEMMs whose tiles do not fill the 148 SMs
  * split K across CTAs (up to ws_bytes / (n*m*4) slices, <= 16): each slice
  * stores its raw int32/fp32 partial sums, a finishing kernel sums the slices
  * in slice order (exact for INT8, so results stay bit-identical;

@@ -76,7 +76,10 @@ struct Cfg {
   static constexpr bool LIFT = LIFT_ != 0;
   static_assert(!LIFT || SPARSE, "in-SM lifting feeds the sparse kernel");
   static constexpr int LIFT_WARPS = LIFT ? 2 : 0;
-  static constexpr int ACC_STAGES = MSUB == 1 ? 2 : 1;
+  // double-buffered accumulators where two (and the sparse metadata
+  // columns) fit the 512 TMEM columns: one-subtile tiles up to 224 tokens
+  // (sparse) / 256 (dense); 256-token sparse tiles drain in between
+  static constexpr int ACC_STAGES = MSUB == 1 && 2 * BN + (SPARSE ? 8 : 0) <= 512 ? 2 : 1;
   static constexpr int EPI_WARPS = 4 * MSUB;
   static constexpr int THREADS = 64 + 32 * (EPI_WARPS + LIFT_WARPS);
   static constexpr int BM = 256 * MSUB;   // weight rows per pair tile
@@ -1037,18 +1040,35 @@ int num_sms() {
   return sms;
 }
 
-// Split-K factor for decode-shaped M: the S minimising ceil(tiles*S/clusters)/S
-// (waves per unit of per-tile work; S = 1 unless a split strictly helps), at
-// most `cap` (workspace slices) and at least 2 k-blocks per slice. Env
-// SLSP_GEMM_KSPLIT forces it (within the same bounds).
-int choose_ksplit(int tiles, int num_kb, int clusters, int cap) {
+// Split-K factor for decode-shaped M: the S minimising the estimated time
+// (S = 1 unless a split strictly helps), at most `cap` (workspace slices) and
+// at least 2 k-blocks per slice. Env SLSP_GEMM_KSPLIT forces it (within the
+// same bounds).
+// split-K applies up to this many tokens (where the tiles can leave SMs
+// idle: decode and moderate prefill chunks); above 256 tokens the workspace
+// is capped at kSplitWsCap bytes (8 slices below that).
+constexpr int64_t kSplitMaxM = 1024;
+constexpr int64_t kSplitWsCap = int64_t{64} << 20;
+
+int choose_ksplit(int tiles, int num_kb, int clusters, int cap, int64_t slice_bytes) {
   const int hi = cap < num_kb / 2 ? cap : num_kb / 2;
   const int forced = static_cast<int>(env_knob("SLSP_GEMM_KSPLIT", 0));
   if (forced > 0) return forced < hi ? forced : (hi > 1 ? hi : 1);
+  // cost in k-block (ring stage) times (~0.27 us each): waves x k-blocks per
+  // slice, plus the measured price of splitting — a fixed ~kSplitCostKb
+  // k-blocks (finish kernel, more tile prologues) and the slices' write +
+  // read traffic at ~5 TB/s, ~kSliceBytesPerKb bytes per k-block time.
+  // Measured on the Qwen2.5-7B shapes: the K = 3584 layers
+  // (21 INT8 / 42 BF16 k-blocks) lose with any split at M <= 256, K = 18944
+  // (111 / 222) gains 1.3-1.6x at M <= 256, ~1.1x at M = 512, and loses at
+  // M = 768 (a 3-way split there cost 1.5x).
+  constexpr int kSplitCostKb = 32;
+  constexpr double kSliceBytesPerKb = 1.35e6;
   int best = 1;
-  double best_cost = static_cast<double>((tiles + clusters - 1) / clusters);
+  double best_cost = static_cast<double>((tiles + clusters - 1) / clusters) * num_kb;
   for (int sp = 2; sp <= hi; ++sp) {
-    const double cost = static_cast<double>((tiles * sp + clusters - 1) / clusters) / sp;
+    const double cost = static_cast<double>((tiles * sp + clusters - 1) / clusters) * ((num_kb + sp - 1) / sp) +
+                        kSplitCostKb + 2.0 * sp * static_cast<double>(slice_bytes) / kSliceBytesPerKb;
     if (cost < best_cost - 1e-9) {
       best_cost = cost;
       best = sp;
@@ -1121,7 +1141,7 @@ int run(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const 
   if constexpr (!C::REG_EPI && !C::LIFT) {
     const int64_t slice = p.n * p.m * 4;
     const int cap = p.ws && slice > 0 ? static_cast<int>(p.ws_cap / slice < 16 ? p.ws_cap / slice : 16) : 1;
-    if (p.m <= 256 && cap > 1) p.ksplit = choose_ksplit(tiles, p.num_kb, clusters, cap);
+    if (p.m <= kSplitMaxM && cap > 1) p.ksplit = choose_ksplit(tiles, p.num_kb, clusters, cap, slice);
   }
   if (p.ksplit > 1) tiles *= p.ksplit;
   if (clusters > tiles) clusters = tiles;
@@ -1153,10 +1173,11 @@ int run_out_cl(int out_mode, const CUtensorMap& a, const CUtensorMap& b, const C
 template <bool SPARSE, MmaKind K, int BN, int LIFT = 0>
 int run_out(int out_mode, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const CUtensorMap& o,
             const Params& p, cudaStream_t s, uint32_t msub, uint32_t kh = 0) {
-  if constexpr (BN >= 128 && SPARSE && !LIFT && K != MmaKind::F16)
+  constexpr bool two_sub = BN >= 128 && !(SPARSE && BN > 224);  // two accumulators fit TMEM
+  if constexpr (two_sub && SPARSE && !LIFT && K != MmaKind::F16)
     if (msub == 2 && kh && out_mode == SLSP_OUT_BF16_NM)
       return run_out_cl<SPARSE, K, BN, 2, 0, 1>(out_mode, a, b, e, o, p, s);
-  if constexpr (BN >= 128)
+  if constexpr (two_sub)
     if (msub == 2) return run_out_cl<SPARSE, K, BN, 2, LIFT, 0>(out_mode, a, b, e, o, p, s);
   return run_out_cl<SPARSE, K, BN, 1, LIFT, 0>(out_mode, a, b, e, o, p, s);
 }
@@ -1168,6 +1189,14 @@ constexpr int kDenseBN = 256;
 constexpr int kDecodeBN = 64;
 constexpr uint32_t kSparseKHalf = 0;  // env SLSP_GEMM_KHALF
 constexpr int64_t kDecodeM = 64;
+// Moderate M: 256-token sparse tiles (one subtile, single-buffered
+// accumulator) where they need fewer token tiles than 224-token ones — each
+// token tile re-streams the whole weight matrix (M = 256: 1 tile instead of
+// 2; M = 512: 2 instead of 3) — and there are at most two waves of them (the
+// accumulator drain between a cluster's tiles is exposed). Measured on the
+// Qwen2.5-7B shapes at M = 256-2048, DESIGN.md §6. Env SLSP_GEMM_BN256_MAXM.
+constexpr int64_t kBn256MaxM = 1024;
+constexpr int kSparseBN256 = 256;
 constexpr uint32_t kDenseMsub = 1;
 constexpr uint32_t kRasterGroup = 16;  // measured best of {4, 8, 16, 32, 148} on Qwen2.5-7B shapes
 
@@ -1218,8 +1247,12 @@ int sparse_entry(int dtype, const void* values, const uint8_t* meta, int64_t n, 
   Params p{};
 
   const bool decode = !LIFT && m <= kDecodeM;
-  const int bn = decode ? kDecodeBN : kSparseBN;
-  const uint32_t msub = decode ? 1u : env_knob("SLSP_GEMM_MSUB", sparse_msub(n, m)) == 2 ? 2u : 1u;
+  const bool wide = !LIFT && !decode && m <= static_cast<int64_t>(env_knob("SLSP_GEMM_BN256_MAXM", kBn256MaxM)) &&
+                    (m + kSparseBN256 - 1) / kSparseBN256 < (m + kSparseBN - 1) / kSparseBN &&
+                    (n + 255) / 256 * ((m + kSparseBN256 - 1) / kSparseBN256) <= num_sms();
+  const int bn = decode ? kDecodeBN : wide ? kSparseBN256 : kSparseBN;
+  const uint32_t msub =
+      (decode || wide) ? 1u : env_knob("SLSP_GEMM_MSUB", sparse_msub(n, m)) == 2 ? 2u : 1u;
   // half k-stages: the two-subtile BF16 [N][M] config of the 8-bit kinds
   const uint32_t kh = (!LIFT && !decode && msub == 2 && esz == 1 && out_mode == SLSP_OUT_BF16_NM &&
                        env_knob("SLSP_GEMM_KHALF", kSparseKHalf))
@@ -1254,6 +1287,11 @@ int sparse_entry(int dtype, const void* values, const uint8_t* meta, int64_t n, 
       if (dtype == SLSP_DT_BF16) return run_out<true, MmaKind::F16, kDecodeBN>(out_mode, ta, tb, te, to, p, s, 1);
       return run_out<true, MmaKind::F8, kDecodeBN>(out_mode, ta, tb, te, to, p, s, 1);
     }
+    if (wide) {
+      if (dtype == SLSP_DT_I8) return run_out<true, MmaKind::I8, kSparseBN256>(out_mode, ta, tb, te, to, p, s, 1);
+      if (dtype == SLSP_DT_BF16) return run_out<true, MmaKind::F16, kSparseBN256>(out_mode, ta, tb, te, to, p, s, 1);
+      return run_out<true, MmaKind::F8, kSparseBN256>(out_mode, ta, tb, te, to, p, s, 1);
+    }
     if (dtype == SLSP_DT_BF16) return run_out<true, MmaKind::F16, kSparseBN>(out_mode, ta, tb, te, to, p, s, msub);
   }
   if (dtype == SLSP_DT_I8) return run_out<true, MmaKind::I8, kSparseBN, L>(out_mode, ta, tb, te, to, p, s, msub, kh);
@@ -1277,7 +1315,11 @@ int slsp_sparse_gemm_ws(int dtype, const void* values, const uint8_t* meta, int6
                              ws_bytes);
 }
 
-int64_t slsp_gemm_workspace_bytes(int64_t n, int64_t m) { return m <= 256 ? 8 * n * m * 4 : 0; }
+int64_t slsp_gemm_workspace_bytes(int64_t n, int64_t m) {
+  if (m > kSplitMaxM) return 0;
+  const int64_t full = 8 * n * m * 4;  // 8 slices
+  return m <= 256 || full <= kSplitWsCap ? full : (kSplitWsCap / (n * m * 4) >= 2 ? kSplitWsCap : 0);
+}
 
 int slsp_sparse_gemm_x(int dtype, const void* values, const uint8_t* meta, int64_t n, int64_t kx, const void* act,
                        int64_t m, const float* s_ch, const float* s_tok, int out_mode, void* out, int64_t ldo,

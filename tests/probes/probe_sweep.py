@@ -155,6 +155,7 @@ def main():
     ap.add_argument("--mn", action="store_true", help="token-major [M][N] output")
     ap.add_argument("--burst", action="store_true", help="bench.py regime: single launches after L2 flushes")
     ap.add_argument("--check", action="store_true", help="compare each sparse config's int32 output with the first")
+    ap.add_argument("--bf16", action="store_true", help="BF16 weights/activations (kind f16) instead of INT8")
     a = ap.parse_args()
     global BURST, CLEAN
     BURST = a.burst
@@ -164,14 +165,24 @@ def main():
     for layer in a.layers.split(","):
         n, k = SHAPES[layer]
         gen = torch.Generator(device="cuda").manual_seed(0)
-        w = slsp.magnitude_prune(torch.randint(-127, 128, (n, k), dtype=torch.int8, device="cuda", generator=gen), 6, 8)
         x = (torch.rand(m, k, device="cuda", generator=gen) * 2 - 1).to(torch.bfloat16)
-        pw = slsp.pack_compress(w, 6, 8)
-        payload, s_tok = slsp.fused_quant_slide(x, 6, 8)
-        q, q_s = slsp.quantize_rows(x)
-        s_ch = torch.rand(n, device="cuda") * 0.01
+        if a.bf16:
+            w = slsp.magnitude_prune((torch.rand(n, k, device="cuda", generator=gen) * 2 - 1).to(torch.bfloat16), 6, 8)
+            pw = slsp.pack_compress(w, 6, 8)
+            payload, s_tok = slsp.lift_rows(x, 6, 8, kp=pw.kp), None
+            q, q_s = x, None
+            s_ch = None
+        else:
+            w = slsp.magnitude_prune(torch.randint(-127, 128, (n, k), dtype=torch.int8, device="cuda", generator=gen),
+                                     6, 8)
+            pw = slsp.pack_compress(w, 6, 8)
+            payload, s_tok = slsp.fused_quant_slide(x, 6, 8)
+            q, q_s = slsp.quantize_rows(x)
+            s_ch = torch.rand(n, device="cuda") * 0.01
         out = torch.empty((m, n) if a.mn else (n, m), dtype=torch.bfloat16, device="cuda")
         om = slsp.OUT_BF16_MN if a.mn else slsp.OUT_BF16_NM
+        if a.bf16:  # no scales: fp32 accumulators out
+            out, om = torch.empty((n, m), dtype=torch.float32, device="cuda"), slsp.OUT_RAW_NM
         flops = 2.0 * m * n * k
         ref = None
         if a.lift:
@@ -202,7 +213,7 @@ def main():
                 elif kind == "sparse":
                     fn = lambda: slsp.sparse_gemm(pw, payload, s_ch=s_ch, s_tok=s_tok, out_mode=om, out=out)
                 else:
-                    fn = lambda: slsp.dense_gemm(w, q.view(torch.int8), s_ch=s_ch, s_tok=q_s,
+                    fn = lambda: slsp.dense_gemm(w, q if a.bf16 else q.view(torch.int8), s_ch=s_ch, s_tok=q_s,
                                                  out_mode=om, out=out)
                 runs.append((kind, kv, fn))
         # round-robin over the configs so every config sees the same thermal/power history

@@ -34,8 +34,12 @@ def run_sparse_raw(slsp, vals, codes, payload, kp, n, z=6, l=8):
     return slsp.sparse_gemm(pw, act).cpu().numpy()
 
 
-@pytest.mark.parametrize("n,k,m", [(256, 256, 224), (512, 1024, 448), (300, 400, 250), (1024, 2048, 700)])
+@pytest.mark.parametrize("n,k,m", [(256, 256, 224), (512, 1024, 448), (300, 400, 250), (1024, 2048, 700),
+                                   (512, 1024, 512), (384, 4096, 256), (256, 2048, 1000), (256, 16384, 256)])
 def test_sparse_int8_bit_exact(slsp, orc, n, k, m):
+    """Token counts cover every tile shape: 224-token tiles (one or two weight
+    subtiles), 256-token tiles (moderate M where they need fewer token tiles:
+    250, 256, 512, 700, 1000) and split-K on them (k = 16384, one tile)."""
     rng = np.random.default_rng(n + k + m)
     w, x, vals, codes, payload, scales, kp = sparse_case(orc, rng, n, k, m)
     got = run_sparse_raw(slsp, vals, codes, payload, kp, n)
@@ -152,7 +156,8 @@ def test_full_shape_sparse_equals_dense(slsp):
     assert torch.equal(ys, yd)
 
 
-@pytest.mark.parametrize("n,k,m", [(512, 1024, 448), (300, 2048, 64), (768, 4096, 1)])
+@pytest.mark.parametrize("n,k,m", [(512, 1024, 448), (300, 2048, 64), (768, 4096, 1), (512, 1024, 256),
+                                   (256, 1024, 500)])
 def test_sparse_bf16_within_tolerance(slsp, n, k, m):
     """BF16 6:8 weights (kind::f16 .sp, one metadata column per K=32 MMA) and
     lifted BF16 activations (lift_row, quantize.hpp:72-89) vs a float64
@@ -174,19 +179,20 @@ def test_sparse_bf16_within_tolerance(slsp, n, k, m):
     assert torch.all((yd - want).abs() <= 2.0 ** -14 * absum + 1e-30)
 
 
-@pytest.mark.parametrize("m", [1, 16, 64])
+@pytest.mark.parametrize("m", [1, 16, 64, 600])
 def test_decode_split_k_int8_bit_exact(slsp, orc, m):
-    """Decode-shaped M: the tiles do not fill the GPU, so K is split across
-    CTAs and int32 partial sums are added atomically — exact, so the result is
-    still bit-identical to the oracle (gemm.hpp:199-233)."""
+    """Decode-shaped and moderate M: the tiles do not fill the GPU, so K is
+    split across CTAs (long K: 96 k-blocks), slices store int32 partial sums
+    and a finishing kernel adds them in order — exact, so the result is still
+    bit-identical to the oracle (gemm.hpp:199-233)."""
     rng = np.random.default_rng(m)
-    n, k = 1024, 4096
+    n, k = 1024, 16384
     w, x, vals, codes, payload, scales, kp = sparse_case(orc, rng, n, k, m)
     got = run_sparse_raw(slsp, vals, codes, payload, kp, n)
     assert np.array_equal(got, orc.sparse_gemm_words(vals, codes, payload))
 
 
-@pytest.mark.parametrize("m", [1, 16, 64])
+@pytest.mark.parametrize("m", [1, 16, 64, 512])
 def test_decode_split_k_bf16_epilogue_identical(slsp, m):
     """BF16 outputs of a split-K GEMM (workspace + finishing kernel) equal the
     unsplit GEMM's bit for bit (INT8: same int32 sums, same fp32 epilogue)."""
@@ -201,7 +207,7 @@ def test_decode_split_k_bf16_epilogue_identical(slsp, m):
     payload, s_tok = slsp.fused_quant_slide(x, 6, 8)
     q, q_s = slsp.quantize_rows(x)
     outs = {}
-    for ks in ("1", "0"):  # forced unsplit, then the automatic split
+    for ks in ("1", "4"):  # forced unsplit, then a 4-way split
         os.environ["SLSP_GEMM_KSPLIT"] = ks
         try:
             for mode in (slsp.OUT_BF16_NM, slsp.OUT_BF16_MN):
@@ -212,7 +218,7 @@ def test_decode_split_k_bf16_epilogue_identical(slsp, m):
     torch.cuda.synchronize()
     for mode in (slsp.OUT_BF16_NM, slsp.OUT_BF16_MN):
         for kind in ("s", "d"):
-            assert torch.equal(outs[("1", mode, kind)].view(torch.int16), outs[("0", mode, kind)].view(torch.int16))
+            assert torch.equal(outs[("1", mode, kind)].view(torch.int16), outs[("4", mode, kind)].view(torch.int16))
 
 
 @pytest.mark.parametrize("z,l,n,k,m", [(6, 8, 512, 1024, 300), (4, 6, 256, 600, 100), (6, 8, 3584, 3584, 8192)])
