@@ -1189,6 +1189,20 @@ constexpr int kDenseBN = 256;
 constexpr int kDecodeBN = 64;
 constexpr uint32_t kSparseKHalf = 0;  // env SLSP_GEMM_KHALF
 constexpr int64_t kDecodeM = 64;
+// 64 < M <= 128: the 64-token tiles too, when they at most fill the machine
+// once (2 token tiles per weight tile) and K is short (<= 8 KB of original
+// weight row): the larger tile count beats re-streaming the weights twice
+// (Qwen2.5-7B qkv/o and 4096x4096 at M = 96/128: 16.5 vs 20.5 us, sparse and
+// dense alike); long-K or wide layers keep the 224/256-token tiles.
+constexpr int64_t kDecodeM2 = 128;
+constexpr int64_t kDecodeKBytes = 8192;
+
+bool decode_tiles(int64_t n, int64_t m, int64_t k_bytes, const char* env) {
+  const int64_t lim = static_cast<int64_t>(env_knob(env, kDecodeM));
+  if (m <= lim) return true;
+  if (m > kDecodeM2 || lim != kDecodeM) return false;
+  return k_bytes <= kDecodeKBytes && (n + 255) / 256 * ((m + kDecodeBN - 1) / kDecodeBN) <= num_sms() / 2;
+}
 // Moderate M: 256-token sparse tiles (one subtile, single-buffered
 // accumulator) where they need fewer token tiles than 224-token ones — each
 // token tile re-streams the whole weight matrix (M = 256: 1 tile instead of
@@ -1246,7 +1260,7 @@ int sparse_entry(int dtype, const void* values, const uint8_t* meta, int64_t n, 
   CUtensorMap ta, tb, te, to;
   Params p{};
 
-  const bool decode = !LIFT && m <= kDecodeM;
+  const bool decode = !LIFT && decode_tiles(n, m, kp * esz * 2 / 3, "SLSP_GEMM_DECODE_M");
   const bool wide = !LIFT && !decode && m <= static_cast<int64_t>(env_knob("SLSP_GEMM_BN256_MAXM", kBn256MaxM)) &&
                     (m + kSparseBN256 - 1) / kSparseBN256 < (m + kSparseBN - 1) / kSparseBN &&
                     (n + 255) / 256 * ((m + kSparseBN256 - 1) / kSparseBN256) <= num_sms();
@@ -1352,7 +1366,7 @@ int slsp_dense_gemm_ws(int dtype, const void* w, int64_t n, int64_t k, const voi
   CUtensorMap ta, tb, to;
   Params p{};
   if ((st = make_map_2d(&ta, w, k * esz, n, 128))) return st;
-  const bool decode = m <= kDecodeM;
+  const bool decode = decode_tiles(n, m, k * esz, "SLSP_DGEMM_DECODE_M");
   const int bn = decode ? kDecodeBN : kDenseBN;
   const uint32_t msub = decode ? 1u : env_knob("SLSP_DGEMM_MSUB", kDenseMsub) == 2 ? 2u : 1u;
   if (workspace && ws_bytes >= 2 * n * m * 4) {  // split-K partial-sum slices

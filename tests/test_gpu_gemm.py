@@ -35,11 +35,13 @@ def run_sparse_raw(slsp, vals, codes, payload, kp, n, z=6, l=8):
 
 
 @pytest.mark.parametrize("n,k,m", [(256, 256, 224), (512, 1024, 448), (300, 400, 250), (1024, 2048, 700),
-                                   (512, 1024, 512), (384, 4096, 256), (256, 2048, 1000), (256, 16384, 256)])
+                                   (512, 1024, 512), (384, 4096, 256), (256, 2048, 1000), (256, 16384, 256),
+                                   (384, 2048, 120)])
 def test_sparse_int8_bit_exact(slsp, orc, n, k, m):
     """Token counts cover every tile shape: 224-token tiles (one or two weight
     subtiles), 256-token tiles (moderate M where they need fewer token tiles:
-    250, 256, 512, 700, 1000) and split-K on them (k = 16384, one tile)."""
+    250, 256, 512, 700, 1000), split-K on them (k = 16384, one tile) and
+    64-token tiles at M = 120 (short K, few weight tiles)."""
     rng = np.random.default_rng(n + k + m)
     w, x, vals, codes, payload, scales, kp = sparse_case(orc, rng, n, k, m)
     got = run_sparse_raw(slsp, vals, codes, payload, kp, n)
@@ -157,7 +159,7 @@ def test_full_shape_sparse_equals_dense(slsp):
 
 
 @pytest.mark.parametrize("n,k,m", [(512, 1024, 448), (300, 2048, 64), (768, 4096, 1), (512, 1024, 256),
-                                   (256, 1024, 500)])
+                                   (256, 1024, 500), (256, 2048, 100)])
 def test_sparse_bf16_within_tolerance(slsp, n, k, m):
     """BF16 6:8 weights (kind::f16 .sp, one metadata column per K=32 MMA) and
     lifted BF16 activations (lift_row, quantize.hpp:72-89) vs a float64
