@@ -527,6 +527,10 @@ int launch_row(ActArgs& a, cudaStream_t s, int* st) {
   // (measured on the Qwen/Llama K values: 1 quad per thread up to 256 quads,
   // then 2 up to 1024, then 4)
   int qpt = nquads <= 256 ? 1 : nquads <= 1024 ? 2 : nquads <= 4096 ? 4 : 0;
+  if (const char* e = std::getenv("SLSP_LIFT_QPT")) {  // perf probing
+    const int f = std::atoi(e);
+    if ((f == 1 || f == 2 || f == 4) && qpt) qpt = f;
+  }
   if (qpt && qpt < QMIN) qpt = QMIN;
   if (qpt && nquads > 1024 * qpt) qpt = 0;
   if (!qpt || nquads == 0) return 0;
