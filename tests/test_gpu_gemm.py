@@ -105,13 +105,15 @@ def test_sparse_bf16_dequant_epilogue(slsp, orc, mode):
     assert np.array_equal(got, want)
 
 
-def test_sparse_fp8_within_tolerance(slsp, orc):
+@pytest.mark.parametrize("m", [448, 250, 120])
+def test_sparse_fp8_within_tolerance(slsp, orc, m):
     """FP8 e4m3 weights and activations, fp32 accumulation in TMEM vs the
     double oracle on decoded values. Stated tolerance: |err| <= 2^-14 * sum|w*x|
     per output (products of e4m3 values are exact in fp32; the bound covers the
-    tensor core's fp32 accumulation order over K'/2 = 768 products)."""
+    tensor core's fp32 accumulation order over K'/2 = 768 products). M covers
+    the 224-token (two-subtile), 256-token and 64-token tile configs."""
     rng = np.random.default_rng(23)
-    n, k, m = 512, 1024, 448
+    n, k = 512, 1024
     mask = compliant_matrix(rng, n, k // 8, 6, 8) != 0
     wf = np.where(mask, rng.uniform(-1, 1, size=mask.shape), 0.0)
     wcode = np.array([orc.fp8_encode(v) for v in (wf * 200).ravel()], np.uint8).reshape(n, k)
@@ -268,12 +270,16 @@ def test_half_k_stage_config_identical(slsp, kind):
     pw = slsp.pack_compress(w, 6, 8)
     payload, s_tok = slsp.fused_quant_slide(x, 6, 8, kind=qk)
     outs = []
-    for kh in ("0", "1"):
-        os.environ["SLSP_GEMM_KHALF"] = kh
-        try:
-            outs.append(slsp.sparse_gemm(pw, payload, s_ch=s_ch, s_tok=s_tok, out_mode=slsp.OUT_BF16_NM))
-        finally:
-            del os.environ["SLSP_GEMM_KHALF"]
+    os.environ["SLSP_GEMM_BN256_MAXM"] = "0"  # keep M = 1000 on the two-subtile tiles half k-stages apply to
+    try:
+        for kh in ("0", "1"):
+            os.environ["SLSP_GEMM_KHALF"] = kh
+            try:
+                outs.append(slsp.sparse_gemm(pw, payload, s_ch=s_ch, s_tok=s_tok, out_mode=slsp.OUT_BF16_NM))
+            finally:
+                del os.environ["SLSP_GEMM_KHALF"]
+    finally:
+        del os.environ["SLSP_GEMM_BN256_MAXM"]
     torch.cuda.synchronize()
     if kind == "int8":
         assert torch.equal(outs[0].view(torch.int16), outs[1].view(torch.int16))
