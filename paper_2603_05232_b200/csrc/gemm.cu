@@ -1174,9 +1174,12 @@ template <bool SPARSE, MmaKind K, int BN, int LIFT = 0>
 int run_out(int out_mode, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const CUtensorMap& o,
             const Params& p, cudaStream_t s, uint32_t msub, uint32_t kh = 0) {
   constexpr bool two_sub = BN >= 128 && !(SPARSE && BN > 224);  // two accumulators fit TMEM
-  if constexpr (two_sub && SPARSE && !LIFT && K != MmaKind::F16)
-    if (msub == 2 && kh && out_mode == SLSP_OUT_BF16_NM)
-      return run_out_cl<SPARSE, K, BN, 2, 0, 1>(out_mode, a, b, e, o, p, s);
+  if constexpr (BN >= 128 && SPARSE && !LIFT && K != MmaKind::F16) {
+    if (kh && msub == 1) return run_out_cl<SPARSE, K, BN, 1, 0, 1>(out_mode, a, b, e, o, p, s);
+    if constexpr (two_sub)
+      if (kh && msub == 2 && out_mode == SLSP_OUT_BF16_NM)
+        return run_out_cl<SPARSE, K, BN, 2, 0, 1>(out_mode, a, b, e, o, p, s);
+  }
   if constexpr (two_sub)
     if (msub == 2) return run_out_cl<SPARSE, K, BN, 2, LIFT, 0>(out_mode, a, b, e, o, p, s);
   return run_out_cl<SPARSE, K, BN, 1, LIFT, 0>(out_mode, a, b, e, o, p, s);
@@ -1211,6 +1214,9 @@ bool decode_tiles(int64_t n, int64_t m, int64_t k_bytes, const char* env) {
 // Qwen2.5-7B shapes at M = 256-2048, DESIGN.md §6. Env SLSP_GEMM_BN256_MAXM.
 constexpr int64_t kBn256MaxM = 1024;
 constexpr int kSparseBN256 = 256;
+// half k-stages on one-subtile tiles (env SLSP_GEMM_KHALF1): measured 6-16%
+// faster at M = 256-1000 on the Qwen2.5-7B shapes, bit-identical
+constexpr uint32_t kSparseKHalf1 = 1;
 constexpr uint32_t kDenseMsub = 1;
 constexpr uint32_t kRasterGroup = 16;  // measured best of {4, 8, 16, 32, 148} on Qwen2.5-7B shapes
 
@@ -1268,8 +1274,13 @@ int sparse_entry(int dtype, const void* values, const uint8_t* meta, int64_t n, 
   const uint32_t msub =
       (decode || wide) ? 1u : env_knob("SLSP_GEMM_MSUB", sparse_msub(n, m)) == 2 ? 2u : 1u;
   // half k-stages: the two-subtile BF16 [N][M] config of the 8-bit kinds
-  const uint32_t kh = (!LIFT && !decode && msub == 2 && esz == 1 && out_mode == SLSP_OUT_BF16_NM &&
-                       env_knob("SLSP_GEMM_KHALF", kSparseKHalf))
+  // half k-stages: the two-subtile BF16 [N][M] config (off by default), and
+  // every one-subtile 8-bit config below the large-M regime (on: a 7-8
+  // stage ring instead of 3-4 for the weight-stream-heavy moderate M)
+  const uint32_t kh = !LIFT && !decode && esz == 1 &&
+                              ((msub == 2 && out_mode == SLSP_OUT_BF16_NM &&
+                                env_knob("SLSP_GEMM_KHALF", kSparseKHalf)) ||
+                               (msub == 1 && env_knob("SLSP_GEMM_KHALF1", kSparseKHalf1)))
                           ? 1u
                           : 0u;
   if (ws && ws_bytes >= 2 * n * m * 4) {  // split-K partial-sum slices
@@ -1302,9 +1313,9 @@ int sparse_entry(int dtype, const void* values, const uint8_t* meta, int64_t n, 
       return run_out<true, MmaKind::F8, kDecodeBN>(out_mode, ta, tb, te, to, p, s, 1);
     }
     if (wide) {
-      if (dtype == SLSP_DT_I8) return run_out<true, MmaKind::I8, kSparseBN256>(out_mode, ta, tb, te, to, p, s, 1);
+      if (dtype == SLSP_DT_I8) return run_out<true, MmaKind::I8, kSparseBN256>(out_mode, ta, tb, te, to, p, s, 1, kh);
       if (dtype == SLSP_DT_BF16) return run_out<true, MmaKind::F16, kSparseBN256>(out_mode, ta, tb, te, to, p, s, 1);
-      return run_out<true, MmaKind::F8, kSparseBN256>(out_mode, ta, tb, te, to, p, s, 1);
+      return run_out<true, MmaKind::F8, kSparseBN256>(out_mode, ta, tb, te, to, p, s, 1, kh);
     }
     if (dtype == SLSP_DT_BF16) return run_out<true, MmaKind::F16, kSparseBN>(out_mode, ta, tb, te, to, p, s, msub);
   }
