@@ -1269,7 +1269,8 @@ int sparse_entry(int dtype, const void* values, const uint8_t* meta, int64_t n, 
   const bool decode = !LIFT && decode_tiles(n, m, kp * esz * 2 / 3, "SLSP_GEMM_DECODE_M");
   const bool wide = !LIFT && !decode && m <= static_cast<int64_t>(env_knob("SLSP_GEMM_BN256_MAXM", kBn256MaxM)) &&
                     (m + kSparseBN256 - 1) / kSparseBN256 < (m + kSparseBN - 1) / kSparseBN &&
-                    (n + 255) / 256 * ((m + kSparseBN256 - 1) / kSparseBN256) <= num_sms();
+                    (n + 255) / 256 * ((m + kSparseBN256 - 1) / kSparseBN256) <=
+                        static_cast<int64_t>(env_knob("SLSP_GEMM_BN256_WAVES", 2)) * (num_sms() / 2);
   const int bn = decode ? kDecodeBN : wide ? kSparseBN256 : kSparseBN;
   const uint32_t msub =
       (decode || wide) ? 1u : env_knob("SLSP_GEMM_MSUB", sparse_msub(n, m)) == 2 ? 2u : 1u;
