@@ -1214,8 +1214,9 @@ bool decode_tiles(int64_t n, int64_t m, int64_t k_bytes, const char* env) {
 // Qwen2.5-7B shapes at M = 256-2048, DESIGN.md §6. Env SLSP_GEMM_BN256_MAXM.
 constexpr int64_t kBn256MaxM = 1024;
 constexpr int kSparseBN256 = 256;
-// half k-stages on one-subtile tiles (env SLSP_GEMM_KHALF1): measured 6-16%
-// faster at M = 256-1000 on the Qwen2.5-7B shapes, bit-identical
+// half k-stages on one-subtile tiles up to M = 1024 (env SLSP_GEMM_KHALF1):
+// measured 6-16% faster at M = 256-1000 on the Qwen2.5-7B shapes,
+// bit-identical; at M = 8192 one-subtile tiles lose 10-20% with them
 constexpr uint32_t kSparseKHalf1 = 1;
 constexpr uint32_t kDenseMsub = 1;
 constexpr uint32_t kRasterGroup = 16;  // measured best of {4, 8, 16, 32, 148} on Qwen2.5-7B shapes
@@ -1281,7 +1282,7 @@ int sparse_entry(int dtype, const void* values, const uint8_t* meta, int64_t n, 
   const uint32_t kh = !LIFT && !decode && esz == 1 &&
                               ((msub == 2 && out_mode == SLSP_OUT_BF16_NM &&
                                 env_knob("SLSP_GEMM_KHALF", kSparseKHalf)) ||
-                               (msub == 1 && env_knob("SLSP_GEMM_KHALF1", kSparseKHalf1)))
+                               (msub == 1 && m <= kBn256MaxM && env_knob("SLSP_GEMM_KHALF1", kSparseKHalf1)))
                           ? 1u
                           : 0u;
   if (ws && ws_bytes >= 2 * n * m * 4) {  // split-K partial-sum slices
