@@ -1227,7 +1227,16 @@ constexpr uint32_t kRasterGroup = 16;  // measured best of {4, 8, 16, 32, 148} o
 // grid would not have (measured on Qwen2.5-7B shapes).
 uint32_t sparse_msub(int64_t n, int64_t m) {
   if (m <= 256) return 1;  // decode shapes: more weight tiles (split-K runs on one-subtile tiles)
-  return 2;  // measured faster or equal on every Qwen2.5-7B shape at M >= 2048
+  // wave quantization: a two-subtile tile costs ~1.8 one-subtile tiles
+  // (measured); take one-subtile tiles only when their waves are clearly
+  // cheaper (Qwen2.5-7B qkv at M = 2048: 90 two-subtile tiles = 1.2 waves on
+  // 74 clusters, 0.041 ms, vs 180 one-subtile tiles 0.039 ms); otherwise two
+  // (faster or equal on every Qwen2.5-7B shape at M = 8192)
+  const int64_t clusters = num_sms() / 2;
+  const int64_t nt = (m + kSparseBN - 1) / kSparseBN;
+  const int64_t w2 = ((n + 511) / 512 * nt + clusters - 1) / clusters;
+  const int64_t w1 = ((n + 255) / 256 * nt + clusters - 1) / clusters;
+  return 10 * w1 < 9 * 18 * w2 / 10 ? 1 : 2;
 }
 
 
