@@ -1,5 +1,6 @@
-"""Runs one Qwen2.5-7B gate_up GEMM (sparse or dense, M=8192) a few times — a
-minimal target for `ncu -k regex:gemm_kernel` captures (perf probing)."""
+"""Runs one Qwen2.5-7B GEMM (sparse or dense; layer and M from argv, default
+gate_up at M=8192) a few times — a minimal target for `ncu -k
+regex:gemm_kernel` captures (perf probing)."""
 import sys
 from pathlib import Path
 
@@ -11,7 +12,7 @@ import paper_2603_05232_b200 as slsp  # noqa: E402
 kind = sys.argv[1] if len(sys.argv) > 1 else "sparse"
 layer = sys.argv[2] if len(sys.argv) > 2 else "gate_up"
 n, k = {"gate_up": (37888, 3584), "down": (3584, 18944), "qkv": (4608, 3584), "o": (3584, 3584)}[layer]
-m = 8192
+m = int(sys.argv[3]) if len(sys.argv) > 3 else 8192
 g = torch.Generator(device="cuda").manual_seed(0)
 w = slsp.magnitude_prune(torch.randint(-127, 128, (n, k), dtype=torch.int8, device="cuda", generator=g), 6, 8)
 x = (torch.rand(m, k, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
