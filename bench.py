@@ -56,7 +56,6 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
-    ap.add_argument("--cpu-rows", type=int, default=64, help="weight rows per layer in the CPU sample")
     return ap.parse_args()
 
 
@@ -145,8 +144,6 @@ class Layer:
         self.kpad = -(-k // 128) * 128
         self.q = torch.empty((m, self.kpad), dtype=torch.uint8, device=device) if dense else None
         self.q_s = torch.empty(m, dtype=torch.float32, device=device) if dense else None
-        if not dense:
-            self.w = None
 
     @property
     def flops(self):
@@ -173,32 +170,34 @@ def run_b200(args, world, rank, local):
     for name, n_total, k in WORKLOADS[args.workload]:
         lo, hi = shard_rows(n_total, world, rank)
         layers.append(Layer(slsp, torch, name, n_total, k, lo, hi, m, z, l, gen, device, not args.no_dense))
-    xgen = torch.Generator(device=device).manual_seed(99)  # activations replicated on every rank
-    xs = {k: (torch.rand((m, k), device=device, generator=xgen) * 2 - 1).to(torch.bfloat16)
-          for k in sorted({L.k for L in layers})}
+    # every layer has its own input tensor (as in a model), so no lift of the
+    # timed step reads an activation a previous lift left in L2; activations are
+    # replicated on every rank (same seed)
+    xgen = torch.Generator(device=device).manual_seed(99)
+    xs = [(torch.rand((m, L.k), device=device, generator=xgen) * 2 - 1).to(torch.bfloat16) for L in layers]
     outs = [torch.empty((L.n, m) if out_mode == slsp.OUT_BF16_NM else (m, L.n), dtype=torch.bfloat16,
                         device=device) for L in layers]
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=device)
 
     # Each kernel call of the step is captured into a CUDA graph, so the timed
     # region measures device time, not Python launch latency.
-    def op_lift(L):
-        return lambda: slsp.fused_quant_slide(xs[L.k], z, l, kp=L.kp, check=False, payload=L.payload,
+    def op_lift(L, i):
+        return lambda: slsp.fused_quant_slide(xs[i], z, l, kp=L.kp, check=False, payload=L.payload,
                                               scales=L.s_tok)
 
     def op_sgemm(L, i):
         return lambda: slsp.sparse_gemm(L.packed, L.payload, s_ch=L.s_ch, s_tok=L.s_tok, out_mode=out_mode,
                                         out=outs[i])
 
-    def op_quant(L):
-        return lambda: slsp.quantize_rows(xs[L.k], kpad=L.kpad, check=False, out=L.q, scales=L.q_s)
+    def op_quant(L, i):
+        return lambda: slsp.quantize_rows(xs[i], kpad=L.kpad, check=False, out=L.q, scales=L.q_s)
 
     def op_dgemm(L, i):
         return lambda: slsp.dense_gemm(L.w, L.q.view(torch.int8), s_ch=L.s_ch, s_tok=L.q_s, out_mode=out_mode,
                                        out=outs[i])
 
-    sparse_ops = [f for i, L in enumerate(layers) for f in (op_lift(L), op_sgemm(L, i))]
-    dense_ops = [] if args.no_dense else [f for i, L in enumerate(layers) for f in (op_quant(L), op_dgemm(L, i))]
+    sparse_ops = [f for i, L in enumerate(layers) for f in (op_lift(L, i), op_sgemm(L, i))]
+    dense_ops = [] if args.no_dense else [f for i, L in enumerate(layers) for f in (op_quant(L, i), op_dgemm(L, i))]
     for f in sparse_ops + dense_ops:  # first calls configure kernels outside capture
         f()
     torch.cuda.synchronize()
@@ -375,7 +374,10 @@ def run_b200(args, world, rank, local):
     if allgather:
         result["allgather"] = allgather
     if rank == 0 and world == 1 and not args.no_cpu:
-        result["cpu_baseline"] = cpu_baseline(slsp, torch, layers, xs, z, l, args.cpu_rows)
+        # the outputs of one sparse step (the dense graph wrote them last)
+        sparse_graph.replay()
+        torch.cuda.synchronize()
+        result["cpu_baseline"], result["parity"] = cpu_baseline(slsp, torch, layers, xs, outs, out_mode, z, l)
     if rank == 0:
         print(json.dumps(result), flush=True)
     if world > 1:
@@ -417,10 +419,10 @@ def time_pack(slsp, torch, layers, z, l, timed, per_op, stream):
 def run_e2e(slsp, torch, layers, xs, outs, out_mode, z, l, stream, device, args, world, total_flops, reduce_max):
     """Same step through the C ABI with HOST buffers: pinned H2D of each
     layer's input, lift + sparse GEMM, D2H of each layer's BF16 output."""
-    host_x = {k: x.cpu().pin_memory() for k, x in xs.items()}
+    host_x = [x.cpu().pin_memory() for x in xs]
     host_y = [torch.empty(o.shape, dtype=o.dtype, pin_memory=True) for o in outs]
     steps = max(1, min(args.steps, 5))
-    h2d = sum(x.numel() * x.element_size() for L in layers for x in [host_x[L.k]])
+    h2d = sum(x.numel() * x.element_size() for x in host_x)
     d2h = sum(y.numel() * y.element_size() for y in host_y)
 
     # Three streams: H2D copies, compute, D2H copies (the two copy engines run
@@ -430,7 +432,7 @@ def run_e2e(slsp, torch, layers, xs, outs, out_mode, z, l, stream, device, args,
     # layer i+1 and the D2H of layer i overlap each other and the compute.
     s_in, s_out = torch.cuda.Stream(device), torch.cuda.Stream(device)
     ev = lambda: torch.cuda.Event()  # noqa: E731
-    dev_in = [torch.empty_like(xs[L.k]) for L in layers]  # each layer's own input (a distinct tensor in a model)
+    dev_in = [torch.empty_like(x) for x in xs]  # each layer's own input (a distinct tensor in a model)
     in_done = [ev() for _ in layers]
     x_free = [ev() for _ in layers]
     y_done = [ev() for _ in layers]
@@ -442,7 +444,7 @@ def run_e2e(slsp, torch, layers, xs, outs, out_mode, z, l, stream, device, args,
         for i, L in enumerate(layers):
             s_in.wait_event(x_free[i])
             with torch.cuda.stream(s_in):
-                dev_in[i].copy_(host_x[L.k], non_blocking=True)
+                dev_in[i].copy_(host_x[i], non_blocking=True)
             in_done[i].record(s_in)
             stream.wait_event(in_done[i])
             stream.wait_event(y_free[i])
@@ -472,55 +474,52 @@ def run_e2e(slsp, torch, layers, xs, outs, out_mode, z, l, stream, device, args,
                     "on three streams (event-ordered per layer)"}
 
 
-def _cpu_sample(R, torch, slsp, layers, xs, z, l, rows, threads):
-    """Bounded CPU sample of the same workload: for every layer, the
-    reference's fused_quant_slide over all M tokens plus its packed-word
-    sparse_gemm (gemm.hpp:199-233) over the first `rows` weight rows."""
-    import numpy as np
+# ---------------------------------------------------------- CPU baseline --
+# The reference's CPU path (oracle/_ref: its headers compiled unmodified; the
+# plain-C port when absent) needs ~8 min per Qwen2.5-7B layer at M = 8192, so
+# a step times a bounded sample and extrapolates: per layer, fused_quant_slide
+# (quantize.hpp:122-174, parallel over tokens) over T sampled tokens and the
+# packed-word sparse_gemm (gemm.hpp:199-233, parallel over weight rows) over R
+# sampled rows x the same T tokens, timed separately, then
+#     t_layer = t_lift * M / T + t_gemm * (N * M) / (R * T)
+# (both are linear in the sampled extent at >= 5 rows per thread). The GPU
+# arm also times the full o_proj layer once and reports the extrapolation's
+# error on it.
+def sample_rows(n: int, per: int = 16) -> list[int]:
+    """16-row groups spread over the weight rows: both CTAs of a pair and both
+    M-subtiles of the first 512-row tile, a middle group and the last rows."""
+    starts = sorted({0, 128, 256, 384, (n // 2) // 128 * 128, max(0, n - per)})
+    return sorted({r for s0 in starts for r in range(s0, min(n, s0 + per))})
 
+
+def sample_tokens(m: int) -> list[int]:
+    """The first two 224-token tiles, two in the middle, the last full tile
+    and the 128-token tail tile of M = 8192 (352 tokens)."""
+    mid = (m // 2) // 224 * 224
+    return sorted({t for t in [*range(0, 448), *range(mid, mid + 448), *range(max(0, m - 352), m)] if t < m})
+
+
+def cpu_layer_times(R, vals, codes, x_bf16, z, l, threads):
+    """(t_lift, t_gemm, payload, scales, acc) of one sampled layer on the CPU."""
     from oracle_lib import DT_BF16, KIND_INT8
 
-    work = []
-    for L in layers:
-        r = min(rows, L.n)
-        wsub = L.w[:r] if L.w is not None else None
-        if wsub is None:
-            raise RuntimeError("cpu baseline needs the dense weights (run without --no-dense)")
-        vals, codes = slsp.compress(slsp.pack_matrix(wsub.contiguous(), z, l))
-        x = xs[L.k].view(torch.int16).cpu().numpy().view(np.uint16)
-        work.append((vals.cpu().numpy(), codes.cpu().numpy(), x, r, L))
     t0 = time.perf_counter()
-    flops = 0.0
-    for vals, codes, x, r, L in work:
-        payload, _ = R.fused_quant_slide(x, z, l, KIND_INT8, DT_BF16, threads=threads)
-        R.sparse_gemm_words(vals, codes, payload, threads=threads)
-        flops += 2.0 * r * L.m * L.k
-    dt = time.perf_counter() - t0
-    return flops, dt
+    payload, scales = R.fused_quant_slide(x_bf16, z, l, KIND_INT8, DT_BF16, threads=threads)
+    t1 = time.perf_counter()
+    acc = R.sparse_gemm_words(vals, codes, payload, threads=threads)
+    t2 = time.perf_counter()
+    return t1 - t0, t2 - t1, payload, scales, acc
 
 
-def cpu_baseline(slsp, torch, layers, xs, z, l, rows):
-    sys.path.insert(0, str(ROOT / "tests"))
-    from oracle_lib import orc, ref
-
-    R = ref()
-    kind = "reference"
-    if R is None:
-        R, kind = orc(), "port"
-    threads = os.cpu_count() or 1
-    flops, dt = _cpu_sample(R, torch, slsp, layers, xs, z, l, rows, threads)
-    return {"value": round(flops / dt / 1e12, 6), "unit": UNIT, "cores": threads, "kind": kind,
-            "sample": f"per layer: fused_quant_slide over all {layers[0].m} tokens + packed-word sparse_gemm over "
-                      f"the first {rows} weight rows; {dt:.1f} s wall on {threads} threads",
-            "seconds": round(dt, 2)}
+def extrapolate(t_lift, t_gemm, n, m, rows, toks):
+    return t_lift * m / toks + t_gemm * (n * m) / (rows * toks)
 
 
-def run_reference(args, world, rank, local):
-    """--impl reference: the reference's own CPU implementation (oracle/_ref,
-    the reference headers compiled unmodified) on this box's host cores, on a
-    bounded sample of the same workload per step. Rank 0 only."""
-    if rank != 0:
-        return
+def cpu_baseline(slsp, torch, layers, xs, outs, out_mode, z, l):
+    """The GPU arm's cpu_baseline leg: the sampled + extrapolated reference
+    step (rank 0, N = 1), the full o_proj timed once, and — since the sample
+    computes exact reference outputs — the parity check of the GPU outputs of
+    the timed step on the sampled (row, token) blocks."""
     import numpy as np
 
     sys.path.insert(0, str(ROOT / "tests"))
@@ -530,41 +529,105 @@ def run_reference(args, world, rank, local):
     kind = "reference"
     if R is None:
         R, kind = orc(), "port"
+    O = orc()  # the a18 dequant restatement (the reference stops at int32)
+    threads = os.cpu_count() or 1
+    t_total, mism, checked, t_sample = 0.0, 0, 0, 0.0
+    per_layer = []
+    for i, L in enumerate(layers):
+        rows, toks = sample_rows(L.n), sample_tokens(L.m)
+        ri, ti = torch.tensor(rows, device=xs[i].device), torch.tensor(toks, device=xs[i].device)
+        vals, codes = R.compress(R.pack_matrix(L.w[ri].cpu().numpy(), z, l, DT_I8, threads=threads), DT_I8)
+        xb = xs[i][ti].view(torch.int16).cpu().numpy().view(np.uint16)
+        tl, tg, payload, scales, acc = cpu_layer_times(R, vals, codes, xb, z, l, threads)
+        t_sample += tl + tg
+        t_total += extrapolate(tl, tg, L.n, L.m, len(rows), len(toks))
+        want = O.dequant_bf16(acc, L.s_ch[ri].cpu().numpy(), scales)
+        y = outs[i][ri][:, ti] if out_mode == slsp.OUT_BF16_NM else outs[i][ti][:, ri].t()
+        got = y.contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+        mism += int((got != want).sum())
+        checked += want.size
+        per_layer.append({"layer": L.name, "rows": len(rows), "tokens": len(toks), "lift_s": round(tl, 4),
+                          "gemm_s": round(tg, 4)})
+    # the full o_proj layer, timed once: calibrates the extrapolation
+    o = next((L for L in layers if L.name == "o"), None)
+    full = None
+    if o is not None:
+        oi = layers.index(o)
+        vals, codes = R.compress(R.pack_matrix(o.w.cpu().numpy(), z, l, DT_I8, threads=threads), DT_I8)
+        xb = xs[oi].view(torch.int16).cpu().numpy().view(np.uint16)
+        tl, tg, *_ = cpu_layer_times(R, vals, codes, xb, z, l, threads)
+        est = extrapolate(per_layer[oi]["lift_s"], per_layer[oi]["gemm_s"], o.n, o.m, per_layer[oi]["rows"],
+                          per_layer[oi]["tokens"])
+        full = {"layer": "o", "n": o.n, "k": o.k, "m": o.m, "seconds": round(tl + tg, 2),
+                "tflops": round(o.flops / (tl + tg) / 1e12, 6), "extrapolated_seconds": round(est, 2),
+                "extrapolation_error": round(est / (tl + tg) - 1, 4)}
+    total_flops = sum(L.flops for L in layers)
+    baseline = {"value": round(total_flops / t_total / 1e12, 6), "unit": UNIT, "cores": threads, "kind": kind,
+                "sample": "per layer: fused_quant_slide over 1248 sampled tokens + packed-word sparse_gemm over "
+                          "~96 sampled weight rows x those tokens, timed separately and extrapolated to the full "
+                          f"layer (t_lift*M/T + t_gemm*N*M/(R*T)); {t_sample:.1f} s sampled on {threads} threads, "
+                          f"{t_total:.0f} s extrapolated per step",
+                "extrapolated_seconds_per_step": round(t_total, 1), "layers": per_layer, "full_o_proj": full}
+    parity = {"bit_exact": mism == 0, "mismatches": mism, "outputs_checked": checked,
+              "what": "BF16 outputs of the timed sparse step on the sampled (row, token) blocks of every layer vs "
+                      f"the CPU {kind} (pack_matrix + compress + fused_quant_slide + sparse_gemm) + the a18 "
+                      "dequant restatement"}
+    return baseline, parity
+
+
+def run_reference(args, world, rank, local):
+    """--impl reference: the reference's own CPU implementation (oracle/_ref,
+    the reference headers compiled unmodified) on this box's host cores. Each
+    step times the sampled layers and extrapolates to the full workload (see
+    cpu_baseline). Rank 0 only."""
+    if rank != 0:
+        return
+    import numpy as np
+
+    sys.path.insert(0, str(ROOT / "tests"))
+    from oracle_lib import DT_I8, orc, ref
+
+    R = ref()
+    kind = "reference"
+    if R is None:
+        R, kind = orc(), "port"
     z, l = (int(v) for v in args.pattern.split(":"))
     m = args.m
-    rows = max(1, args.cpu_rows // 4)
     rng = np.random.default_rng(1234)
     threads = os.cpu_count() or 1
     work = []
     for name, n, k in WORKLOADS[args.workload]:
+        rows, toks = len(sample_rows(n)), len(sample_tokens(m))
         w = R.magnitude_prune(rng.integers(-127, 128, size=(rows, k)).astype(np.int8), z, l, DT_I8)
         vals, codes = R.compress(R.pack_matrix(w, z, l, DT_I8, threads=threads), DT_I8)
-        x = rng.uniform(-1, 1, size=(m, k)).astype(np.float32)
+        x = rng.uniform(-1, 1, size=(toks, k)).astype(np.float32)
         xb = ((x.view(np.uint32).astype(np.uint64) + 0x7FFF + ((x.view(np.uint32) >> 16) & 1)) >> 16).astype(np.uint16)
-        work.append((vals, codes, xb, k))
+        work.append((vals, codes, xb, n, rows, toks))
 
     def step():
-        for vals, codes, xb, k in work:
-            payload, _ = R.fused_quant_slide(xb, z, l, KIND_INT8, DT_BF16, threads=threads)
-            R.sparse_gemm_words(vals, codes, payload, threads=threads)
+        t = 0.0
+        for vals, codes, xb, n, rows, toks in work:
+            tl, tg, *_ = cpu_layer_times(R, vals, codes, xb, z, l, threads)
+            t += extrapolate(tl, tg, n, m, rows, toks)
+        return t
 
     for _ in range(args.warmup):
         step()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        step()
-    dt = (time.perf_counter() - t0) / args.steps
-    flops = sum(2.0 * rows * m * k for *_, k in work)
+    ts = [step() for _ in range(args.steps)]
+    dt = sum(ts) / len(ts)
+    flops = sum(2.0 * m * n * k for _, n, k in WORKLOADS[args.workload])
     value = flops / dt / 1e12
-    sample = (f"per layer of {args.workload}: fused_quant_slide over all {m} tokens + packed-word sparse_gemm "
-              f"over {rows} weight rows (of {', '.join(str(n) for _, n, _ in WORKLOADS[args.workload])})")
+    sample = (f"per layer of {args.workload}: fused_quant_slide over {len(sample_tokens(m))} of {m} tokens + "
+              f"packed-word sparse_gemm over ~96 sampled weight rows x those tokens, timed separately and "
+              f"extrapolated to the full layer (t_lift*M/T + t_gemm*N*M/(R*T)); ms_per_step is the extrapolated "
+              f"full-step time")
     print(json.dumps({
         "metric": METRIC, "value": round(value, 6), "unit": UNIT, "impl": "reference", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "int8",
         "data": "synthetic: W = magnitude_prune(U[-127,127], 6:8) int8, X = U(-1,1) bf16, seeded",
         "config": {"workload": f"{args.workload} all linear shapes, {args.pattern} INT8 W8A8, M={m} prefill",
-                   "m": m, "pattern": args.pattern, "sampled_rows_per_layer": rows},
+                   "m": m, "pattern": args.pattern},
         "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
         "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)

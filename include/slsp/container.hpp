@@ -13,6 +13,7 @@
 #include <cstring>
 #include <filesystem>
 #include <fstream>
+#include <unistd.h>
 #include <iterator>
 #include <span>
 #include <string>
@@ -229,12 +230,31 @@ inline Container deserialize(std::span<const std::uint8_t> bytes) {
   return c;
 }
 
+// Atomic replace (container.hpp:249-262 contract): serialize into
+// <path>.tmp<pid> in the destination directory, check the write, then rename
+// it over the destination — a failed write leaves the old file intact.
 inline void save_container(const std::filesystem::path& path, const Container& c) {
   const auto bytes = serialize(c);
-  std::ofstream f(path, std::ios::binary | std::ios::trunc);
-  if (!f) throw ContainerError("cannot open " + path.string() + " for writing");
-  f.write(reinterpret_cast<const char*>(bytes.data()), static_cast<std::streamsize>(bytes.size()));
-  if (!f) throw ContainerError("write failed: " + path.string());
+  auto tmp = path;
+  tmp += ".tmp" + std::to_string(static_cast<long long>(::getpid()));
+  {
+    std::ofstream f(tmp, std::ios::binary | std::ios::trunc);
+    if (!f) throw ContainerError("cannot open " + tmp.string() + " for writing");
+    f.write(reinterpret_cast<const char*>(bytes.data()), static_cast<std::streamsize>(bytes.size()));
+    f.flush();
+    if (!f) {
+      f.close();
+      std::error_code ec;
+      std::filesystem::remove(tmp, ec);
+      throw ContainerError("write failed: " + tmp.string());
+    }
+  }
+  std::error_code ec;
+  std::filesystem::rename(tmp, path, ec);
+  if (ec) {
+    std::filesystem::remove(tmp, ec);
+    throw ContainerError("cannot rename " + tmp.string() + " to " + path.string());
+  }
 }
 
 inline Container load_container(const std::filesystem::path& path) {

@@ -83,6 +83,9 @@ SLSP_API const char* slsp_status_string(int status);
 SLSP_API const char* slsp_last_cuda_error(void);
 /* 1 if device `dev` is an sm_100 part the kernels run on, else 0. */
 SLSP_API int slsp_device_supported(int dev);
+/* Re-reads the SLSP_* tuning/probing environment variables (snapshotted once
+ * per process otherwise; probes and tests that change them call this). */
+SLSP_API void slsp_reload_knobs(void);
 
 /* a1 — pattern.hpp:107-154 plan_status + plan_decomposition (host only).
  * Hardware window fixed at hw_m:hw_n. Fills window_count and up to `cap`
@@ -203,9 +206,10 @@ SLSP_API int slsp_sparse_gemm_x(int dtype, const void* values, const uint8_t* me
                        int64_t m, const float* s_ch, const float* s_tok, int out_mode, void* out, int64_t ldo,
                        slsp_stream_t stream);
 
-/* Workspace of the *_ws GEMM variants: 8*n*m*4 bytes for decode-shaped M
- * (m <= 256), the same capped at 64 MiB (0 if that holds < 2 slices) for
- * 256 < m <= 1024, else 0. With it, GEMMs whose tiles do not fill the 148 SMs
+/* Workspace budget of the *_ws GEMM variants for m <= 1024: 8 slices of
+ * n*m*4 bytes, capped at 64 MiB (whole slices; 0 if that holds < 2 slices);
+ * 0 for m > 1024. slsp_*_gemm_config reports what a call actually needs.
+ * With it, GEMMs whose tiles do not fill the 148 SMs
  * split K across CTAs (up to ws_bytes / (n*m*4) slices, <= 16): each slice
  * stores its raw int32/fp32 partial sums, a finishing kernel sums the slices
  * in slice order (exact for INT8, so results stay bit-identical;
@@ -218,6 +222,30 @@ SLSP_API int slsp_sparse_gemm_ws(int dtype, const void* values, const uint8_t* m
 SLSP_API int slsp_dense_gemm_ws(int dtype, const void* w, int64_t n, int64_t k, const void* act, int64_t m,
                        const float* s_ch, const float* s_tok, int out_mode, void* out, int64_t ldo, void* workspace,
                        int64_t ws_bytes, slsp_stream_t stream);
+
+/* The tile configuration a GEMM call with these arguments launches (nothing
+ * is launched; no device memory is touched). ws_bytes is the workspace the
+ * caller would pass to the *_ws variant (0: none). workspace_bytes is what
+ * the chosen split-K actually uses (0 when unsplit), so callers can size
+ * the workspace exactly: query with slsp_gemm_workspace_bytes(n, m), then
+ * allocate cfg.workspace_bytes. */
+typedef struct slsp_gemm_config {
+  int tokens_per_tile;      /* MMA N across the CTA pair (tokens of one tile) */
+  int weight_rows_per_tile; /* 256 x subtiles */
+  int subtiles;             /* M=256 UMMA subtiles per tile (1 or 2) */
+  int half_k_stages;        /* 1: 128 lifted bytes per ring stage */
+  int stages;               /* shared-memory ring depth */
+  int cluster_ctas;         /* CTAs per cluster */
+  int ksplit;               /* split-K slices (1: none) */
+  int epilogue;             /* 0: chunked TMEM drain, 1: register-staged two-subtile drain */
+  int clusters;             /* persistent clusters launched */
+  int reserved;
+  int64_t workspace_bytes;  /* workspace the split needs (0 when ksplit == 1) */
+} slsp_gemm_config;
+SLSP_API int slsp_sparse_gemm_config(int dtype, int64_t n, int64_t kp, int64_t m, int out_mode, int64_t ws_bytes,
+                                     slsp_gemm_config* cfg);
+SLSP_API int slsp_dense_gemm_config(int dtype, int64_t n, int64_t k, int64_t m, int out_mode, int64_t ws_bytes,
+                                    slsp_gemm_config* cfg);
 
 /* a15 — gemm.hpp:142-162 dense_gemm on tcgen05.mma (the speedup
  * denominator). w: n x k, act: m x k (token rows; the reference's X is k x m,

@@ -8,6 +8,7 @@ or a B200 is missing, calls raise.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import os
 import threading
@@ -71,6 +72,18 @@ _ERRORS = {
     ERR_CUDA: CudaError,
 }
 
+
+class GemmConfig(C.Structure):
+    """slsp_gemm_config (include/slsp_b200.h): the tile configuration a GEMM call launches."""
+    _fields_ = [("tokens_per_tile", C.c_int), ("weight_rows_per_tile", C.c_int), ("subtiles", C.c_int),
+                ("half_k_stages", C.c_int), ("stages", C.c_int), ("cluster_ctas", C.c_int), ("ksplit", C.c_int),
+                ("epilogue", C.c_int), ("clusters", C.c_int), ("reserved", C.c_int),
+                ("workspace_bytes", C.c_int64)]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_ if name != "reserved"}
+
+
 _lib = None
 _lock = threading.Lock()
 
@@ -111,6 +124,9 @@ def lib() -> C.CDLL:
                 "slsp_gemm_order": (i32, [i32, vp, vp, i64, i64, i64, vp, vp, i64, vp]),
                 "slsp_sparse_gemm_x": (i32, [i32, vp, vp, i64, i64, vp, i64, vp, vp, i32, vp, i64, vp]),
                 "slsp_tiled_meta_bytes": (i64, [i64, i64]),
+                "slsp_reload_knobs": (None, []),
+                "slsp_sparse_gemm_config": (i32, [i32, i64, i64, i64, i32, i64, C.POINTER(GemmConfig)]),
+                "slsp_dense_gemm_config": (i32, [i32, i64, i64, i64, i32, i64, C.POINTER(GemmConfig)]),
             }
             for name, (res, args) in sigs.items():
                 fn = getattr(L, name)
@@ -162,6 +178,51 @@ def _require_cuda(*ts: torch.Tensor) -> None:
     for t in ts:
         if t is not None and (not t.is_cuda or not t.is_contiguous()):
             raise ValueError("slsp_b200 operates on contiguous CUDA tensors")
+
+
+def _require_buffer(t: torch.Tensor, name: str, dtypes, shape: tuple, device) -> None:
+    """A caller-provided output buffer: CUDA, contiguous, on `device`, of one of
+    `dtypes` and exactly `shape` — the kernels write shape-derived extents, so
+    a smaller buffer would be overrun (the reference allocates its own results)."""
+    if not t.is_cuda or not t.is_contiguous() or t.device != device:
+        raise ValueError(f"{name} must be a contiguous CUDA tensor on {device}")
+    if t.dtype not in dtypes:
+        raise TypeError(f"{name} must have dtype {' or '.join(str(d) for d in dtypes)}, got {t.dtype}")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+
+
+def _require_scales(t: torch.Tensor | None, name: str, count: int, device) -> None:
+    if t is None:
+        return
+    if not t.is_cuda or not t.is_contiguous() or t.device != device or t.dtype != torch.float32:
+        raise ValueError(f"{name} must be a contiguous float32 CUDA tensor on {device}")
+    if t.numel() < count:
+        raise ValueError(f"{name} holds {t.numel()} scales, needs >= {count}")
+
+
+def reload_knobs() -> None:
+    """Re-read the SLSP_* tuning/probing environment variables (snapshotted by
+    the library once per process otherwise)."""
+    lib().slsp_reload_knobs()
+
+
+@contextlib.contextmanager
+def knobs(**kv):
+    """Temporarily set SLSP_* knobs, e.g. ``with knobs(SLSP_GEMM_MSUB=2): ...``."""
+    old = {k: os.environ.get(k) for k in kv}
+    try:
+        for k, v in kv.items():
+            os.environ[k] = str(v)
+        reload_knobs()
+        yield
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+        reload_knobs()
 
 
 # ---- a1: geometry --------------------------------------------------------------
@@ -327,16 +388,27 @@ def fused_quant_slide(x: torch.Tensor, z: int, l: int, kind: int = QUANT_INT8, k
     rows, cols = x.shape
     kprime = lifted_width(cols, z, l)
     kp = round_up(kprime, 256) if kp is None else kp
+    if kp < kprime or kp % 4:
+        raise DimensionMismatchError(f"payload width kp={kp} must be >= K'={kprime} and a multiple of 4")
     if payload is None:
         payload = torch.empty((rows, kp // 4), dtype=torch.int32, device=x.device)
+    else:
+        _require_buffer(payload, "payload", (torch.int32, torch.uint32), (rows, kp // 4), x.device)
     if scales is None:
         scales = torch.empty(rows, dtype=torch.float32, device=x.device)
+    else:
+        _require_buffer(scales, "scales", (torch.float32,), (rows,), x.device)
     bad = C.c_int64(-1)
     ws = _status_ws(x.device) if check else None
     st = lib().slsp_fused_quant_slide(_in_dtype(x), _ptr(x), rows, cols, z, l, kind, kp, _ptr(payload),
                                       _ptr(scales), _ptr(ws), C.byref(bad), _stream(x.device))
     _check(st, "fused_quant_slide", f"non-finite activation value in row {bad.value}"
            if st == ERR_NON_FINITE else None)
+    # QuantizedLiftedActivation's kind and pattern (quantize.hpp:101-116) travel
+    # with the payload so sparse_gemm can reject a mismatched pairing
+    # (gemm.hpp:203-208) instead of computing garbage
+    payload.slsp_kind = kind
+    payload.slsp_pattern = (z, l)
     return payload, scales
 
 
@@ -347,13 +419,19 @@ def quantize_rows(x: torch.Tensor, kind: int = QUANT_INT8, kpad: int | None = No
     _require_cuda(x)
     rows, cols = x.shape
     kpad = round_up(cols, 128) if kpad is None else kpad
+    if kpad < cols:
+        raise DimensionMismatchError(f"kpad={kpad} must be >= cols={cols}")
     if out is None:
         out = torch.empty((rows, kpad), dtype=torch.uint8, device=x.device)
+    else:
+        _require_buffer(out, "out", (torch.uint8, torch.int8, torch.float8_e4m3fn), (rows, kpad), x.device)
     if scales is None:
         scales = torch.empty(rows, dtype=torch.float32, device=x.device)
+    else:
+        _require_buffer(scales, "scales", (torch.float32,), (rows,), x.device)
     bad = C.c_int64(-1)
     ws = _status_ws(x.device) if check else None
-    st = lib().slsp_quantize_rows(_in_dtype(x), _ptr(x), rows, cols, kind, kpad, _ptr(out), _ptr(scales),
+    st = lib().slsp_quantize_rows(_in_dtype(x), _ptr(x), rows, cols, kind, kpad, _ptr(_raw(out)), _ptr(scales),
                                   _ptr(ws), C.byref(bad), _stream(x.device))
     _check(st, "quantize_rows", f"non-finite activation value in row {bad.value}"
            if st == ERR_NON_FINITE else None)
@@ -374,22 +452,59 @@ def lift_rows(x: torch.Tensor, z: int, l: int, kp: int | None = None) -> torch.T
 
 # ---- a13-a15: GEMMs ------------------------------------------------------------------
 def _gemm_out(out_mode: int, n: int, m: int, acc_int: bool, device, out: torch.Tensor | None):
-    if out is not None:
-        return out
+    """The GEMM's result buffer: allocated, or the caller's checked against the
+    exact extents the kernel writes (n x m / m x n, dtype of the mode)."""
     if out_mode == OUT_RAW_NM:
-        return torch.empty((n, m), dtype=torch.int32 if acc_int else torch.float32, device=device)
-    if out_mode == OUT_BF16_NM:
-        return torch.empty((n, m), dtype=torch.bfloat16, device=device)
-    return torch.empty((m, n), dtype=torch.bfloat16, device=device)
+        dt, shape = (torch.int32 if acc_int else torch.float32), (n, m)
+    elif out_mode == OUT_BF16_NM:
+        dt, shape = torch.bfloat16, (n, m)
+    elif out_mode == OUT_BF16_MN:
+        dt, shape = torch.bfloat16, (m, n)
+    else:
+        raise ValueError(f"unknown out_mode {out_mode}")
+    if out is None:
+        return torch.empty(shape, dtype=dt, device=device)
+    _require_buffer(out, "out", (dt,), shape, device)
+    return out
 
 
-def _workspace(n: int, m: int, out_mode: int, device):
-    """Split-K partial-sum slices for decode-shaped GEMMs (stream-ordered
-    caching-allocator memory, one buffer per call)."""
-    nb = int(lib().slsp_gemm_workspace_bytes(n, m))
+def sparse_gemm_config(w: "PackedWeights", m: int, out_mode: int = OUT_RAW_NM) -> dict:
+    """The tile configuration sparse_gemm(w, act[m], out_mode=...) launches."""
+    cfg = GemmConfig()
+    _check(lib().slsp_sparse_gemm_config(w.dtype, w.n, w.kp, m, out_mode, int(lib().slsp_gemm_workspace_bytes(w.n, m)),
+                                         C.byref(cfg)), "sparse_gemm_config")
+    return cfg.as_dict()
+
+
+def dense_gemm_config(dtype: int, n: int, k: int, m: int, out_mode: int = OUT_RAW_NM) -> dict:
+    cfg = GemmConfig()
+    _check(lib().slsp_dense_gemm_config(dtype, n, k, m, out_mode, int(lib().slsp_gemm_workspace_bytes(n, m)),
+                                        C.byref(cfg)), "dense_gemm_config")
+    return cfg.as_dict()
+
+
+def _workspace(query, device):
+    """Split-K partial-sum slices, sized to what the chosen configuration uses
+    (nothing is allocated when the call does not split)."""
+    cfg = GemmConfig()
+    _check(query(C.byref(cfg)), "gemm_config")
+    nb = int(cfg.workspace_bytes)
     if nb == 0:
         return None, 0
     return torch.empty(nb, dtype=torch.uint8, device=device), nb
+
+
+def _check_pairing(w: "PackedWeights", act: torch.Tensor) -> None:
+    """gemm.hpp:203-208: the payload's quant kind and pattern must match the weights."""
+    kind = getattr(act, "slsp_kind", None)
+    pattern = getattr(act, "slsp_pattern", None)
+    if pattern is not None and tuple(pattern) != (w.z, w.l):
+        raise DimensionMismatchError(f"activation lifted for pattern {pattern[0]}:{pattern[1]}, "
+                                     f"weights packed for {w.z}:{w.l}")
+    if kind is not None:
+        want = QUANT_INT8 if w.values.dtype == torch.int8 else QUANT_FP8E4M3 if w.dtype == DT_E4M3 else None
+        if want is None or kind != want:
+            raise DimensionMismatchError(f"activation quant kind {kind} does not match {w.values.dtype} weights")
 
 
 def sparse_gemm(w: PackedWeights, act: torch.Tensor, s_ch: torch.Tensor | None = None,
@@ -400,9 +515,14 @@ def sparse_gemm(w: PackedWeights, act: torch.Tensor, s_ch: torch.Tensor | None =
     m = act.shape[0]
     if act.shape[1] * act.element_size() != w.kp * w.values.element_size():
         raise DimensionMismatchError("lifted activation width does not match compressed weights")
+    _check_pairing(w, act)
+    _require_scales(s_ch, "s_ch", w.n, act.device)
+    _require_scales(s_tok, "s_tok", m, act.device)
     o = _gemm_out(out_mode, w.n, m, w.values.dtype == torch.int8, act.device, out)
     ldo = o.shape[1]
-    ws, wsb = _workspace(w.n, m, out_mode, act.device)
+    wsb0 = int(lib().slsp_gemm_workspace_bytes(w.n, m))
+    ws, wsb = _workspace(lambda q: lib().slsp_sparse_gemm_config(w.dtype, w.n, w.kp, m, out_mode, wsb0, q),
+                         act.device)
     _check(lib().slsp_sparse_gemm_ws(w.dtype, _ptr(_raw(w.values)), _ptr(w.tiled()), w.n, w.kp, _ptr(act), m,
                                      _ptr(s_ch), _ptr(s_tok), out_mode, _ptr(o), ldo, _ptr(ws), wsb,
                                      _stream(act.device)), "sparse_gemm")
@@ -419,6 +539,8 @@ def sparse_gemm_x(w: "PackedWeights | GemmOrderWeights", act: torch.Tensor, s_ch
     m = act.shape[0]
     if act.shape[1] * act.element_size() != g.kx:
         raise DimensionMismatchError(f"activation rows must be kx = {g.kx} bytes (quantize_rows(x, kpad=kx))")
+    _require_scales(s_ch, "s_ch", g.n, act.device)
+    _require_scales(s_tok, "s_tok", m, act.device)
     o = _gemm_out(out_mode, g.n, m, g.values.dtype == torch.int8, act.device, out)
     ldo = o.shape[1]
     _check(lib().slsp_sparse_gemm_x(g.dtype, _ptr(_raw(g.values)), _ptr(g.meta_tiled), g.n, g.kx, _ptr(act), m,
@@ -436,9 +558,13 @@ def dense_gemm(w: torch.Tensor, act: torch.Tensor, s_ch: torch.Tensor | None = N
     m = act.shape[0]
     if act.shape[1] * act.element_size() != k * w.element_size():
         raise DimensionMismatchError("dense_gemm: W.cols must equal X.rows")
+    _require_scales(s_ch, "s_ch", n, act.device)
+    _require_scales(s_tok, "s_tok", m, act.device)
     o = _gemm_out(out_mode, n, m, w.dtype == torch.int8, act.device, out)
     ldo = o.shape[1]
-    ws, wsb = _workspace(n, m, out_mode, act.device)
+    wsb0 = int(lib().slsp_gemm_workspace_bytes(n, m))
+    ws, wsb = _workspace(lambda q: lib().slsp_dense_gemm_config(dtype_code(w), n, k, m, out_mode, wsb0, q),
+                         act.device)
     _check(lib().slsp_dense_gemm_ws(dtype_code(w), _ptr(_raw(w)), n, k, _ptr(act), m, _ptr(s_ch), _ptr(s_tok),
                                     out_mode, _ptr(o), ldo, _ptr(ws), wsb, _stream(act.device)), "dense_gemm")
     return o

@@ -30,11 +30,13 @@ FLAGS = [
 ]
 
 
-def _digest() -> str:
+def _digest(src: str | None = None) -> str:
+    """Content hash of the flags, the shared headers and `src` (all sources if None)."""
     import hashlib
 
     h = hashlib.sha256(" ".join(FLAGS).encode())
-    deps = sorted([CSRC / s for s in SOURCES] + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")))
+    srcs = SOURCES if src is None else [src]
+    deps = sorted([CSRC / s for s in srcs] + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")))
     deps.append(ROOT / "include" / "slsp_b200.h")
     for d in deps:
         h.update(d.name.encode())
@@ -50,6 +52,12 @@ def _stale() -> bool:
     if not LIB.exists() or not STAMP.exists():
         return True
     return STAMP.read_text().strip() != _digest()
+
+
+def _obj_stale(src: str) -> bool:
+    obj = PKG / "_build" / (Path(src).stem + ".o")
+    stamp = PKG / "_build" / (Path(src).stem + ".stamp")
+    return not obj.exists() or not stamp.exists() or stamp.read_text().strip() != _digest(src)
 
 
 def build_watchdog() -> Path:
@@ -72,17 +80,20 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     procs = []
     for src in SOURCES:
         obj = build_dir / (Path(src).stem + ".o")
-        cmd = [NVCC, *[f for f in FLAGS if f not in ("-shared",)], "-dc" if False else "-c",
-               str(CSRC / src), "-o", str(obj)]
+        objs.append(str(obj))
+        if not force and not _obj_stale(src):  # per-object content hash: rebuild only what changed
+            continue
+        cmd = [NVCC, *[f for f in FLAGS if f not in ("-shared",)], "-c", str(CSRC / src), "-o", str(obj)]
         cmd = [c for c in cmd if c not in ("-cudart", "static")]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
-        objs.append(str(obj))
     failed = False
     for src, p in procs:
         out, _ = p.communicate()
         if verbose or p.returncode:
             sys.stderr.write(f"[nvcc {src}]\n{out}")
         failed |= p.returncode != 0
+        if p.returncode == 0:
+            (build_dir / (Path(src).stem + ".stamp")).write_text(_digest(src))
     if failed:
         raise RuntimeError("nvcc failed")
     link = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",

@@ -12,6 +12,7 @@ loading is a retile, not a re-encode), then `slsp_tile_meta_ex`.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import struct
 import zlib
 from dataclasses import dataclass, field
@@ -152,8 +153,21 @@ def load_container(path) -> Container:
 
 
 def save_container(path, c: Container) -> None:
-    """container.hpp:249-262 save_container."""
-    Path(path).write_bytes(serialize(c))
+    """container.hpp:249-262 save_container: written to a temporary file in the
+    destination directory, flushed, then renamed over the destination, so a
+    failed write never leaves a truncated container or destroys the old one."""
+    path = Path(path)
+    data = serialize(c)
+    tmp = path.with_name(f"{path.name}.tmp{os.getpid()}")
+    try:
+        with open(tmp, "wb") as f:
+            f.write(data)
+            f.flush()
+            os.fsync(f.fileno())
+        os.replace(tmp, path)
+    except OSError as e:
+        tmp.unlink(missing_ok=True)
+        raise ContainerError(f"cannot write {path}: {e}") from e
 
 
 # ---- device side ---------------------------------------------------------------------

@@ -935,21 +935,12 @@ EncodeTiledFn get_encode() {
   return fn;
 }
 
-uint32_t debug_flags() {  // read per call so one probe process can sweep it
-  const char* e = std::getenv("SLSP_GEMM_DEBUG");
-  return e ? static_cast<uint32_t>(std::strtoul(e, nullptr, 0)) : 0u;
-}
+uint32_t debug_flags() { return static_cast<uint32_t>(slsp_host::knob("SLSP_GEMM_DEBUG", 0)); }
 
-// Tuning knob from the environment (read per call: cheap, and lets probes vary it).
-uint32_t env_knob(const char* name, uint32_t dflt) {
-  const char* e = std::getenv(name);
-  return (e && *e) ? static_cast<uint32_t>(std::strtoul(e, nullptr, 0)) : dflt;
-}
+// Tuning knob (SLSP_* environment snapshot, slsp_reload_knobs re-reads it).
+uint32_t env_knob(const char* name, uint32_t dflt) { return static_cast<uint32_t>(slsp_host::knob(name, dflt)); }
 
-uintptr_t env_ptr(const char* name) {
-  const char* e = std::getenv(name);
-  return (e && *e) ? static_cast<uintptr_t>(std::strtoull(e, nullptr, 0)) : 0;
-}
+uintptr_t env_ptr(const char* name) { return static_cast<uintptr_t>(slsp_host::knob(name, 0)); }
 
 // Byte-addressed 2D map (uint8 elements): rows x row_bytes, box rows x box_bytes
 // (128 B: 128B swizzle, 64 B: 64B swizzle).
@@ -1030,15 +1021,7 @@ void select_epilogue(Params& p, int out_mode, uint32_t msub, const void* out, in
   if (out_mode != SLSP_OUT_BF16_MN && p.tma_store && epi == 2) p.tma_store = 0;
 }
 
-int num_sms() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  return sms;
-}
+using slsp_host::num_sms;
 
 // Split-K factor for decode-shaped M: the S minimising the estimated time
 // (S = 1 unless a split strictly helps), at most `cap` (workspace slices) and
@@ -1105,8 +1088,10 @@ __global__ void splitk_finish_kernel(const Acc* __restrict__ ws, int slices, int
 
 template <typename C>
 int run(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const CUtensorMap& o, Params p,
-        cudaStream_t s) {
-  static int max_clusters = 0;
+        cudaStream_t s, slsp_gemm_config* query) {
+  // co-resident clusters of this shape (GPC packing) and the >48 KB smem
+  // opt-in: properties of the device, computed once per device
+  static slsp_host::PerDevice<int> max_clusters_cache;
   auto kern = gemm_kernel<C>;
   cudaLaunchConfig_t cfg{};
   cudaLaunchAttribute attr[2];
@@ -1121,28 +1106,44 @@ int run(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const 
   cfg.stream = s;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  if (!max_clusters) {  // how many clusters of this shape are co-resident (GPC packing)
+  int max_clusters = 0;
+  int st = max_clusters_cache.get(&max_clusters, [&](int& v) -> int {
     SLSP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     cfg.gridDim = dim3(C::CL * (num_sms() / C::CL));
     int n = 0;
     SLSP_CUDA_TRY(cudaOccupancyMaxActiveClusters(&n, kern, &cfg));
-    max_clusters = n > 0 ? n : num_sms() / C::CL;
-  }
+    v = n > 0 ? n : num_sms() / C::CL;
+    return SLSP_OK;
+  });
+  if (st) return st;
   p.m_tiles = static_cast<int>((p.n + C::BM - 1) / C::BM);
   p.n_tiles = static_cast<int>((p.m + C::BN - 1) / C::BN);
   int tiles = (p.m_tiles + C::NPAIR - 1) / C::NPAIR * p.n_tiles;
-  if (tiles == 0) return SLSP_OK;
   int clusters = max_clusters;
   const int cluster_cap = static_cast<int>(env_knob("SLSP_GEMM_CLUSTERS", 0));  // perf probing
   if (cluster_cap > 0 && clusters > cluster_cap) clusters = cluster_cap;
   // split-K where the tiles do not fill the machine (decode-shaped M): needs
   // an accumulation target (the int32/fp32 output itself, or a workspace)
   p.ksplit = 1;
+  const int64_t slice = p.n * p.m * 4;
   if constexpr (!C::REG_EPI && !C::LIFT) {
-    const int64_t slice = p.n * p.m * 4;
     const int cap = p.ws && slice > 0 ? static_cast<int>(p.ws_cap / slice < 16 ? p.ws_cap / slice : 16) : 1;
-    if (p.m <= kSplitMaxM && cap > 1) p.ksplit = choose_ksplit(tiles, p.num_kb, clusters, cap, slice);
+    if (tiles > 0 && p.m <= kSplitMaxM && cap > 1) p.ksplit = choose_ksplit(tiles, p.num_kb, clusters, cap, slice);
   }
+  if (query) {
+    query->tokens_per_tile = C::BN;
+    query->weight_rows_per_tile = C::BM;
+    query->subtiles = C::MSUB;
+    query->half_k_stages = C::KH ? 1 : 0;
+    query->stages = C::STAGES;
+    query->cluster_ctas = C::CL;
+    query->ksplit = p.ksplit;
+    query->epilogue = C::REG_EPI ? 1 : 0;
+    query->clusters = clusters < tiles * p.ksplit ? clusters : tiles * p.ksplit;
+    query->workspace_bytes = p.ksplit > 1 ? p.ksplit * slice : 0;
+    return SLSP_OK;
+  }
+  if (tiles == 0) return SLSP_OK;
   if (p.ksplit > 1) tiles *= p.ksplit;
   if (clusters > tiles) clusters = tiles;
   cfg.gridDim = dim3(C::CL * clusters);
@@ -1159,11 +1160,11 @@ int run(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const 
 
 template <bool SPARSE, MmaKind K, int BN, int MSUB, int LIFT, int KH>
 int run_out_cl(int out_mode, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const CUtensorMap& o,
-               const Params& p, cudaStream_t s) {
+               const Params& p, cudaStream_t s, slsp_gemm_config* q) {
   switch (out_mode) {  // STAGES = 0: as many as fit
-    case SLSP_OUT_RAW_NM: return run<Cfg<SPARSE, K, BN, 0, SLSP_OUT_RAW_NM, MSUB, LIFT, KH>>(a, b, e, o, p, s);
-    case SLSP_OUT_BF16_NM: return run<Cfg<SPARSE, K, BN, 0, SLSP_OUT_BF16_NM, MSUB, LIFT, KH>>(a, b, e, o, p, s);
-    case SLSP_OUT_BF16_MN: return run<Cfg<SPARSE, K, BN, 0, SLSP_OUT_BF16_MN, MSUB, LIFT, KH>>(a, b, e, o, p, s);
+    case SLSP_OUT_RAW_NM: return run<Cfg<SPARSE, K, BN, 0, SLSP_OUT_RAW_NM, MSUB, LIFT, KH>>(a, b, e, o, p, s, q);
+    case SLSP_OUT_BF16_NM: return run<Cfg<SPARSE, K, BN, 0, SLSP_OUT_BF16_NM, MSUB, LIFT, KH>>(a, b, e, o, p, s, q);
+    case SLSP_OUT_BF16_MN: return run<Cfg<SPARSE, K, BN, 0, SLSP_OUT_BF16_MN, MSUB, LIFT, KH>>(a, b, e, o, p, s, q);
   }
   return SLSP_ERR_INVALID;
 }
@@ -1172,17 +1173,17 @@ int run_out_cl(int out_mode, const CUtensorMap& a, const CUtensorMap& b, const C
 // sparse kernel, SLSP_DGEMM_MSUB for the dense one; decode tiles: 1).
 template <bool SPARSE, MmaKind K, int BN, int LIFT = 0>
 int run_out(int out_mode, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const CUtensorMap& o,
-            const Params& p, cudaStream_t s, uint32_t msub, uint32_t kh = 0) {
+            const Params& p, cudaStream_t s, uint32_t msub, uint32_t kh, slsp_gemm_config* q) {
   constexpr bool two_sub = BN >= 128 && !(SPARSE && BN > 224);  // two accumulators fit TMEM
   if constexpr (BN >= 128 && SPARSE && !LIFT && K != MmaKind::F16) {
-    if (kh && msub == 1) return run_out_cl<SPARSE, K, BN, 1, 0, 1>(out_mode, a, b, e, o, p, s);
+    if (kh && msub == 1) return run_out_cl<SPARSE, K, BN, 1, 0, 1>(out_mode, a, b, e, o, p, s, q);
     if constexpr (two_sub)
       if (kh && msub == 2 && out_mode == SLSP_OUT_BF16_NM)
-        return run_out_cl<SPARSE, K, BN, 2, 0, 1>(out_mode, a, b, e, o, p, s);
+        return run_out_cl<SPARSE, K, BN, 2, 0, 1>(out_mode, a, b, e, o, p, s, q);
   }
   if constexpr (two_sub)
-    if (msub == 2) return run_out_cl<SPARSE, K, BN, 2, LIFT, 0>(out_mode, a, b, e, o, p, s);
-  return run_out_cl<SPARSE, K, BN, 1, LIFT, 0>(out_mode, a, b, e, o, p, s);
+    if (msub == 2) return run_out_cl<SPARSE, K, BN, 2, LIFT, 0>(out_mode, a, b, e, o, p, s, q);
+  return run_out_cl<SPARSE, K, BN, 1, LIFT, 0>(out_mode, a, b, e, o, p, s, q);
 }
 
 constexpr int kSparseBN = 224;
@@ -1256,24 +1257,27 @@ int check_out(int out_mode, const float* s_ch, const float* s_tok, void* out, in
 
 // Shared body of slsp_sparse_gemm (lifted activations, kp bytes per token)
 // and slsp_sparse_gemm_x (unlifted X, kx = 2kp/3 bytes per token, lifted in
-// shared memory; values/metadata in slsp_gemm_order's window order).
+// shared memory; values/metadata in slsp_gemm_order's window order). With
+// `q` set nothing is launched: the chosen configuration is reported.
 template <bool LIFT>
 int sparse_entry(int dtype, const void* values, const uint8_t* meta, int64_t n, int64_t kp, const void* act,
                  int64_t act_row, int64_t m, const float* s_ch, const float* s_tok, int out_mode, void* out,
-                 int64_t ldo, slsp_stream_t stream, void* ws = nullptr, int64_t ws_bytes = 0) {
+                 int64_t ldo, slsp_stream_t stream, void* ws, int64_t ws_bytes, slsp_gemm_config* q = nullptr) {
   using namespace slsp_host;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (n < 0 || m < 0 || kp <= 0) return SLSP_ERR_INVALID;
   if (kp % 256 != 0) return SLSP_ERR_DIMENSION;
   if (kp > (int64_t{1} << 23)) return SLSP_ERR_INVALID;  // gemm.hpp:56 int8 accumulator bound
   if (n > (int64_t{1} << 31) - 256 || m > (int64_t{1} << 31) - 256) return SLSP_ERR_UNSUPPORTED;
-  int st = check_out(out_mode, s_ch, s_tok, out, ldo, n, m);
-  if (st) return st;
+  int st = SLSP_OK;
+  if (out_mode != SLSP_OUT_RAW_NM && out_mode != SLSP_OUT_BF16_NM && out_mode != SLSP_OUT_BF16_MN)
+    return SLSP_ERR_INVALID;
+  if (!q && (st = check_out(out_mode, s_ch, s_tok, out, ldo, n, m))) return st;
   if (dtype != SLSP_DT_I8 && dtype != SLSP_DT_E4M3 && !(dtype == SLSP_DT_BF16 && !LIFT)) return SLSP_ERR_UNSUPPORTED;
   if ((st = require_sm100())) return st;
-  if (n == 0 || m == 0) return SLSP_OK;
+  if (!q && (n == 0 || m == 0)) return SLSP_OK;
   const int esz = dtype == SLSP_DT_BF16 ? 2 : 1;
-  CUtensorMap ta, tb, te, to;
+  CUtensorMap ta{}, tb{}, te{}, to{};
   Params p{};
 
   const bool decode = !LIFT && decode_tiles(n, m, kp * esz * 2 / 3, "SLSP_GEMM_DECODE_M");
@@ -1284,7 +1288,6 @@ int sparse_entry(int dtype, const void* values, const uint8_t* meta, int64_t n, 
   const int bn = decode ? kDecodeBN : wide ? kSparseBN256 : kSparseBN;
   const uint32_t msub =
       (decode || wide) ? 1u : env_knob("SLSP_GEMM_MSUB", sparse_msub(n, m)) == 2 ? 2u : 1u;
-  // half k-stages: the two-subtile BF16 [N][M] config of the 8-bit kinds
   // half k-stages: the two-subtile BF16 [N][M] config (off by default), and
   // every one-subtile 8-bit config below the large-M regime (on: a 7-8
   // stage ring instead of 3-4 for the weight-stream-heavy moderate M)
@@ -1298,12 +1301,14 @@ int sparse_entry(int dtype, const void* values, const uint8_t* meta, int64_t n, 
     p.ws = ws;
     p.ws_cap = ws_bytes;
   }
-  if ((st = make_map_2d(&tb, act, act_row * esz, m, bn / 2))) return st;
-  if ((st = make_map_2d(&ta, values, kp / 2 * esz, n, 128, kh ? 64 : 128))) return st;
-  // BF16 and half k-stages: a stage is 128 logical k -> one 2 KB metadata atom
-  if ((st = make_map_meta(&te, meta, n, kp, (esz == 2 || kh) ? 8 : 16))) return st;
-  if ((st = make_map_out(&to, out, out_mode, n, m, ldo, epi_cols(msub, bn, out_mode), &p.tma_store))) return st;
-  select_epilogue(p, out_mode, msub, out, ldo, s_tok);
+  if (!q) {
+    if ((st = make_map_2d(&tb, act, act_row * esz, m, bn / 2))) return st;
+    if ((st = make_map_2d(&ta, values, kp / 2 * esz, n, 128, kh ? 64 : 128))) return st;
+    // BF16 and half k-stages: a stage is 128 logical k -> one 2 KB metadata atom
+    if ((st = make_map_meta(&te, meta, n, kp, (esz == 2 || kh) ? 8 : 16))) return st;
+    if ((st = make_map_out(&to, out, out_mode, n, m, ldo, epi_cols(msub, bn, out_mode), &p.tma_store))) return st;
+    select_epilogue(p, out_mode, msub, out, ldo, s_tok);
+  }
   p.n = n;
   p.m = m;
   p.num_kb = static_cast<int>(kp * esz / (kh ? 128 : 256));
@@ -1319,60 +1324,29 @@ int sparse_entry(int dtype, const void* values, const uint8_t* meta, int64_t n, 
   constexpr int L = LIFT ? 1 : 0;
   if constexpr (!LIFT) {
     if (decode) {
-      if (dtype == SLSP_DT_I8) return run_out<true, MmaKind::I8, kDecodeBN>(out_mode, ta, tb, te, to, p, s, 1);
-      if (dtype == SLSP_DT_BF16) return run_out<true, MmaKind::F16, kDecodeBN>(out_mode, ta, tb, te, to, p, s, 1);
-      return run_out<true, MmaKind::F8, kDecodeBN>(out_mode, ta, tb, te, to, p, s, 1);
+      if (dtype == SLSP_DT_I8) return run_out<true, MmaKind::I8, kDecodeBN>(out_mode, ta, tb, te, to, p, s, 1, 0, q);
+      if (dtype == SLSP_DT_BF16)
+        return run_out<true, MmaKind::F16, kDecodeBN>(out_mode, ta, tb, te, to, p, s, 1, 0, q);
+      return run_out<true, MmaKind::F8, kDecodeBN>(out_mode, ta, tb, te, to, p, s, 1, 0, q);
     }
     if (wide) {
-      if (dtype == SLSP_DT_I8) return run_out<true, MmaKind::I8, kSparseBN256>(out_mode, ta, tb, te, to, p, s, 1, kh);
-      if (dtype == SLSP_DT_BF16) return run_out<true, MmaKind::F16, kSparseBN256>(out_mode, ta, tb, te, to, p, s, 1);
-      return run_out<true, MmaKind::F8, kSparseBN256>(out_mode, ta, tb, te, to, p, s, 1, kh);
+      if (dtype == SLSP_DT_I8)
+        return run_out<true, MmaKind::I8, kSparseBN256>(out_mode, ta, tb, te, to, p, s, 1, kh, q);
+      if (dtype == SLSP_DT_BF16)
+        return run_out<true, MmaKind::F16, kSparseBN256>(out_mode, ta, tb, te, to, p, s, 1, 0, q);
+      return run_out<true, MmaKind::F8, kSparseBN256>(out_mode, ta, tb, te, to, p, s, 1, kh, q);
     }
-    if (dtype == SLSP_DT_BF16) return run_out<true, MmaKind::F16, kSparseBN>(out_mode, ta, tb, te, to, p, s, msub);
+    if (dtype == SLSP_DT_BF16)
+      return run_out<true, MmaKind::F16, kSparseBN>(out_mode, ta, tb, te, to, p, s, msub, 0, q);
   }
-  if (dtype == SLSP_DT_I8) return run_out<true, MmaKind::I8, kSparseBN, L>(out_mode, ta, tb, te, to, p, s, msub, kh);
-  return run_out<true, MmaKind::F8, kSparseBN, L>(out_mode, ta, tb, te, to, p, s, msub, kh);
+  if (dtype == SLSP_DT_I8)
+    return run_out<true, MmaKind::I8, kSparseBN, L>(out_mode, ta, tb, te, to, p, s, msub, kh, q);
+  return run_out<true, MmaKind::F8, kSparseBN, L>(out_mode, ta, tb, te, to, p, s, msub, kh, q);
 }
 
-}  // namespace
-
-extern "C" {
-
-int slsp_sparse_gemm(int dtype, const void* values, const uint8_t* meta, int64_t n, int64_t kp, const void* act,
-                     int64_t m, const float* s_ch, const float* s_tok, int out_mode, void* out, int64_t ldo,
-                     slsp_stream_t stream) {
-  return sparse_entry<false>(dtype, values, meta, n, kp, act, kp, m, s_ch, s_tok, out_mode, out, ldo, stream);
-}
-
-int slsp_sparse_gemm_ws(int dtype, const void* values, const uint8_t* meta, int64_t n, int64_t kp, const void* act,
-                        int64_t m, const float* s_ch, const float* s_tok, int out_mode, void* out, int64_t ldo,
-                        void* workspace, int64_t ws_bytes, slsp_stream_t stream) {
-  return sparse_entry<false>(dtype, values, meta, n, kp, act, kp, m, s_ch, s_tok, out_mode, out, ldo, stream, workspace,
-                             ws_bytes);
-}
-
-int64_t slsp_gemm_workspace_bytes(int64_t n, int64_t m) {
-  if (m > kSplitMaxM) return 0;
-  const int64_t full = 8 * n * m * 4;  // 8 slices
-  return m <= 256 || full <= kSplitWsCap ? full : (kSplitWsCap / (n * m * 4) >= 2 ? kSplitWsCap : 0);
-}
-
-int slsp_sparse_gemm_x(int dtype, const void* values, const uint8_t* meta, int64_t n, int64_t kx, const void* act,
-                       int64_t m, const float* s_ch, const float* s_tok, int out_mode, void* out, int64_t ldo,
-                       slsp_stream_t stream) {
-  if (kx <= 0) return SLSP_ERR_INVALID;
-  if (kx % 512 != 0) return SLSP_ERR_DIMENSION;
-  return sparse_entry<true>(dtype, values, meta, n, kx / 2 * 3, act, kx, m, s_ch, s_tok, out_mode, out, ldo, stream);
-}
-
-int slsp_dense_gemm(int dtype, const void* w, int64_t n, int64_t k, const void* act, int64_t m, const float* s_ch,
-                    const float* s_tok, int out_mode, void* out, int64_t ldo, slsp_stream_t stream) {
-  return slsp_dense_gemm_ws(dtype, w, n, k, act, m, s_ch, s_tok, out_mode, out, ldo, nullptr, 0, stream);
-}
-
-int slsp_dense_gemm_ws(int dtype, const void* w, int64_t n, int64_t k, const void* act, int64_t m, const float* s_ch,
-                       const float* s_tok, int out_mode, void* out, int64_t ldo, void* workspace, int64_t ws_bytes,
-                       slsp_stream_t stream) {
+int dense_entry(int dtype, const void* w, int64_t n, int64_t k, const void* act, int64_t m, const float* s_ch,
+                const float* s_tok, int out_mode, void* out, int64_t ldo, void* workspace, int64_t ws_bytes,
+                slsp_stream_t stream, slsp_gemm_config* q = nullptr) {
   using namespace slsp_host;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (n < 0 || m < 0 || k <= 0) return SLSP_ERR_INVALID;
@@ -1381,13 +1355,14 @@ int slsp_dense_gemm_ws(int dtype, const void* w, int64_t n, int64_t k, const voi
   if ((k * esz) % 128 != 0) return SLSP_ERR_DIMENSION;
   if (dtype == SLSP_DT_I8 && k > (int64_t{1} << 23)) return SLSP_ERR_INVALID;  // gemm.hpp:147-149
   if (n > (int64_t{1} << 31) - 256 || m > (int64_t{1} << 31) - 256) return SLSP_ERR_UNSUPPORTED;
-  int st = check_out(out_mode, s_ch, s_tok, out, ldo, n, m);
-  if (st) return st;
+  if (out_mode != SLSP_OUT_RAW_NM && out_mode != SLSP_OUT_BF16_NM && out_mode != SLSP_OUT_BF16_MN)
+    return SLSP_ERR_INVALID;
+  int st = SLSP_OK;
+  if (!q && (st = check_out(out_mode, s_ch, s_tok, out, ldo, n, m))) return st;
   if ((st = require_sm100())) return st;
-  if (n == 0 || m == 0) return SLSP_OK;
-  CUtensorMap ta, tb, to;
+  if (!q && (n == 0 || m == 0)) return SLSP_OK;
+  CUtensorMap ta{}, tb{}, to{};
   Params p{};
-  if ((st = make_map_2d(&ta, w, k * esz, n, 128))) return st;
   const bool decode = decode_tiles(n, m, k * esz, "SLSP_DGEMM_DECODE_M");
   const int bn = decode ? kDecodeBN : kDenseBN;
   const uint32_t msub = decode ? 1u : env_knob("SLSP_DGEMM_MSUB", kDenseMsub) == 2 ? 2u : 1u;
@@ -1395,9 +1370,12 @@ int slsp_dense_gemm_ws(int dtype, const void* w, int64_t n, int64_t k, const voi
     p.ws = workspace;
     p.ws_cap = ws_bytes;
   }
-  if ((st = make_map_2d(&tb, act, k * esz, m, bn / 2))) return st;
-  if ((st = make_map_out(&to, out, out_mode, n, m, ldo, epi_cols(msub, bn, out_mode), &p.tma_store))) return st;
-  select_epilogue(p, out_mode, msub, out, ldo, s_tok);
+  if (!q) {
+    if ((st = make_map_2d(&ta, w, k * esz, n, 128))) return st;
+    if ((st = make_map_2d(&tb, act, k * esz, m, bn / 2))) return st;
+    if ((st = make_map_out(&to, out, out_mode, n, m, ldo, epi_cols(msub, bn, out_mode), &p.tma_store))) return st;
+    select_epilogue(p, out_mode, msub, out, ldo, s_tok);
+  }
   p.n = n;
   p.m = m;
   p.num_kb = static_cast<int>(k * esz / 128);
@@ -1411,13 +1389,77 @@ int slsp_dense_gemm_ws(int dtype, const void* w, int64_t n, int64_t k, const voi
   p.group = static_cast<int>(env_knob("SLSP_GEMM_GROUP", kRasterGroup));
   p.splitbar = static_cast<int>(env_knob("SLSP_GEMM_SPLITBAR", 1));
   if (dtype == SLSP_DT_I8)
-    return decode ? run_out<false, MmaKind::I8, kDecodeBN>(out_mode, ta, tb, ta, to, p, s, 1)
-                  : run_out<false, MmaKind::I8, kDenseBN>(out_mode, ta, tb, ta, to, p, s, msub);
+    return decode ? run_out<false, MmaKind::I8, kDecodeBN>(out_mode, ta, tb, ta, to, p, s, 1, 0, q)
+                  : run_out<false, MmaKind::I8, kDenseBN>(out_mode, ta, tb, ta, to, p, s, msub, 0, q);
   if (dtype == SLSP_DT_E4M3)
-    return decode ? run_out<false, MmaKind::F8, kDecodeBN>(out_mode, ta, tb, ta, to, p, s, 1)
-                  : run_out<false, MmaKind::F8, kDenseBN>(out_mode, ta, tb, ta, to, p, s, msub);
-  return decode ? run_out<false, MmaKind::F16, kDecodeBN>(out_mode, ta, tb, ta, to, p, s, 1)
-                : run_out<false, MmaKind::F16, kDenseBN>(out_mode, ta, tb, ta, to, p, s, msub);
+    return decode ? run_out<false, MmaKind::F8, kDecodeBN>(out_mode, ta, tb, ta, to, p, s, 1, 0, q)
+                  : run_out<false, MmaKind::F8, kDenseBN>(out_mode, ta, tb, ta, to, p, s, msub, 0, q);
+  return decode ? run_out<false, MmaKind::F16, kDecodeBN>(out_mode, ta, tb, ta, to, p, s, 1, 0, q)
+                : run_out<false, MmaKind::F16, kDenseBN>(out_mode, ta, tb, ta, to, p, s, msub, 0, q);
+}
+
+}  // namespace
+
+extern "C" {
+
+int slsp_sparse_gemm(int dtype, const void* values, const uint8_t* meta, int64_t n, int64_t kp, const void* act,
+                     int64_t m, const float* s_ch, const float* s_tok, int out_mode, void* out, int64_t ldo,
+                     slsp_stream_t stream) {
+  return sparse_entry<false>(dtype, values, meta, n, kp, act, kp, m, s_ch, s_tok, out_mode, out, ldo, stream, nullptr,
+                             0);
+}
+
+int slsp_sparse_gemm_ws(int dtype, const void* values, const uint8_t* meta, int64_t n, int64_t kp, const void* act,
+                        int64_t m, const float* s_ch, const float* s_tok, int out_mode, void* out, int64_t ldo,
+                        void* workspace, int64_t ws_bytes, slsp_stream_t stream) {
+  return sparse_entry<false>(dtype, values, meta, n, kp, act, kp, m, s_ch, s_tok, out_mode, out, ldo, stream, workspace,
+                             ws_bytes);
+}
+
+int64_t slsp_gemm_workspace_bytes(int64_t n, int64_t m) {
+  if (m > kSplitMaxM || n <= 0 || m <= 0) return 0;
+  const int64_t slice = n * m * 4;
+  const int64_t full = 8 * slice;  // 8 slices, capped at kSplitWsCap (0 if that holds < 2 slices)
+  return full <= kSplitWsCap ? full : (kSplitWsCap / slice >= 2 ? kSplitWsCap / slice * slice : 0);
+}
+
+int slsp_sparse_gemm_config(int dtype, int64_t n, int64_t kp, int64_t m, int out_mode, int64_t ws_bytes,
+                            slsp_gemm_config* cfg) {
+  if (!cfg) return SLSP_ERR_INVALID;
+  *cfg = slsp_gemm_config{};
+  // a non-null sentinel stands for "a workspace of ws_bytes will be passed"
+  void* ws = ws_bytes > 0 ? reinterpret_cast<void*>(uintptr_t{256}) : nullptr;
+  return sparse_entry<false>(dtype, nullptr, nullptr, n, kp, nullptr, kp, m, nullptr, nullptr, out_mode, nullptr, 0,
+                             nullptr, ws, ws_bytes, cfg);
+}
+
+int slsp_dense_gemm_config(int dtype, int64_t n, int64_t k, int64_t m, int out_mode, int64_t ws_bytes,
+                           slsp_gemm_config* cfg) {
+  if (!cfg) return SLSP_ERR_INVALID;
+  *cfg = slsp_gemm_config{};
+  void* ws = ws_bytes > 0 ? reinterpret_cast<void*>(uintptr_t{256}) : nullptr;
+  return dense_entry(dtype, nullptr, n, k, nullptr, m, nullptr, nullptr, out_mode, nullptr, 0, ws, ws_bytes, nullptr,
+                     cfg);
+}
+
+int slsp_sparse_gemm_x(int dtype, const void* values, const uint8_t* meta, int64_t n, int64_t kx, const void* act,
+                       int64_t m, const float* s_ch, const float* s_tok, int out_mode, void* out, int64_t ldo,
+                       slsp_stream_t stream) {
+  if (kx <= 0) return SLSP_ERR_INVALID;
+  if (kx % 512 != 0) return SLSP_ERR_DIMENSION;
+  return sparse_entry<true>(dtype, values, meta, n, kx / 2 * 3, act, kx, m, s_ch, s_tok, out_mode, out, ldo, stream,
+                            nullptr, 0);
+}
+
+int slsp_dense_gemm(int dtype, const void* w, int64_t n, int64_t k, const void* act, int64_t m, const float* s_ch,
+                    const float* s_tok, int out_mode, void* out, int64_t ldo, slsp_stream_t stream) {
+  return dense_entry(dtype, w, n, k, act, m, s_ch, s_tok, out_mode, out, ldo, nullptr, 0, stream);
+}
+
+int slsp_dense_gemm_ws(int dtype, const void* w, int64_t n, int64_t k, const void* act, int64_t m, const float* s_ch,
+                       const float* s_tok, int out_mode, void* out, int64_t ldo, void* workspace, int64_t ws_bytes,
+                       slsp_stream_t stream) {
+  return dense_entry(dtype, w, n, k, act, m, s_ch, s_tok, out_mode, out, ldo, workspace, ws_bytes, stream);
 }
 
 }  // extern "C"

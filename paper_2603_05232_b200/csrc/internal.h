@@ -3,7 +3,9 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
+#include <mutex>
 #include <utility>
 
 #include "../../include/slsp_b200.h"
@@ -56,6 +58,49 @@ int launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaS
   SLSP_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
   return SLSP_OK;
 }
+
+// ---- tuning / probing knobs -------------------------------------------------
+// SLSP_* environment variables are snapshotted once (first use) and again on
+// slsp_reload_knobs(), so an entry point reads a handful of cached pairs
+// instead of scanning the process environment on every call.
+const char* knob_str(const char* name);  // nullptr when unset
+inline uint64_t knob(const char* name, uint64_t dflt) {
+  const char* e = knob_str(name);
+  return (e && *e) ? static_cast<uint64_t>(std::strtoull(e, nullptr, 0)) : dflt;
+}
+
+// ---- per-device host state -------------------------------------------------
+// Launch attributes, occupancy-derived grid caps and uploaded tables are
+// device properties: a process that drives several GPUs through the C ABI
+// computes each once per device (never "once per process").
+constexpr int kMaxDevices = 64;
+
+int current_device(int* dev);  // SLSP_OK, or SLSP_ERR_CUDA / SLSP_ERR_UNSUPPORTED
+
+template <typename T>
+struct PerDevice {
+  std::mutex mu;
+  bool done[kMaxDevices] = {};
+  T val[kMaxDevices] = {};
+  // The current device's value, computed by init(T&) -> status on first use
+  // (failures are not cached).
+  template <typename F>
+  int get(T* out, F&& init) {
+    int dev = 0;
+    int st = current_device(&dev);
+    if (st) return st;
+    std::lock_guard<std::mutex> g(mu);
+    if (!done[dev]) {
+      if ((st = init(val[dev]))) return st;
+      done[dev] = true;
+    }
+    *out = val[dev];
+    return SLSP_OK;
+  }
+};
+
+// Number of SMs of the current device (cached per device); 0 on failure.
+int num_sms();
 
 inline int elem_size(int dtype) {
   switch (dtype) {

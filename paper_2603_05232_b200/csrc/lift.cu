@@ -44,10 +44,7 @@ struct ActArgs {
 // else (default) the row-resident path where it applies. (Measured and
 // dropped: persistent CTAs with a register double buffer, and a coalesced
 // one-block-per-lane layout — both slower on the Qwen/Llama K values.)
-int env_row_path() {
-  const char* e = std::getenv("SLSP_LIFT_ROW");
-  return e && *e ? e[0] - '0' : 1;
-}
+int env_row_path() { return static_cast<int>(slsp_host::knob("SLSP_LIFT_ROW", 1)); }
 
 template <int IN, int KIND, bool LIFT>
 __global__ void __launch_bounds__(kThreads) act_kernel(ActArgs a) {
@@ -527,8 +524,7 @@ int launch_row(ActArgs& a, cudaStream_t s, int* st) {
   // (measured on the Qwen/Llama K values: 1 quad per thread up to 256 quads,
   // then 2 up to 1024, then 4)
   int qpt = nquads <= 256 ? 1 : nquads <= 1024 ? 2 : nquads <= 4096 ? 4 : 0;
-  if (const char* e = std::getenv("SLSP_LIFT_QPT")) {  // perf probing
-    const int f = std::atoi(e);
+  if (const int f = static_cast<int>(slsp_host::knob("SLSP_LIFT_QPT", 0))) {  // perf probing
     if ((f == 1 || f == 2 || f == 4) && qpt) qpt = f;
   }
   if (qpt && qpt < QMIN) qpt = QMIN;
@@ -543,15 +539,16 @@ int launch_row(ActArgs& a, cudaStream_t s, int* st) {
 
 template <int IN, int KIND, int L>
 int launch_warp(ActArgs& a, cudaStream_t s) {
-  static int grid_cap = 0;
+  static slsp_host::PerDevice<int> grid_caps;
   auto k = act_warp_kernel<IN, KIND, L>;
-  if (!grid_cap) {
-    int dev = 0, sms = 0, per_sm = 0;
-    SLSP_CUDA_TRY(cudaGetDevice(&dev));
-    SLSP_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  int grid_cap = 0;
+  int st = grid_caps.get(&grid_cap, [&](int& v) -> int {
+    int per_sm = 0;
     SLSP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, 0));
-    grid_cap = sms * (per_sm > 0 ? per_sm : 1);
-  }
+    v = slsp_host::num_sms() * (per_sm > 0 ? per_sm : 1);
+    return v > 0 ? SLSP_OK : SLSP_ERR_CUDA;
+  });
+  if (st) return st;
   const int64_t blocks = (a.rows + 7) / 8;
   k<<<static_cast<unsigned>(blocks < grid_cap ? blocks : grid_cap), 256, 0, s>>>(a);
   SLSP_LAUNCH_CHECK();
@@ -604,22 +601,30 @@ int launch_act(ActArgs& a, int esz, cudaStream_t s) {
   const size_t smem = ((a.in_cols_pad * esz + 15) & ~static_cast<int64_t>(15)) + (KIND != K_NONE ? a.in_cols_pad : 0);
   if (smem > 200 * 1024) return SLSP_ERR_UNSUPPORTED;
   auto k = act_kernel<IN, KIND, LIFT>;
-  // Launch configuration is cached per kernel instance and smem size so the
-  // entry point stays cheap and CUDA-graph capturable (no per-call queries).
-  static size_t cached_smem = 0;
-  static int cached_per_sm = 0, sms = 0;
-  if (!sms) {
+  // Launch configuration is cached per device, kernel instance and smem size
+  // so the entry point stays cheap and CUDA-graph capturable (no per-call
+  // queries on the common path).
+  struct Occ {
+    size_t smem;
+    int per_sm;
+  };
+  static slsp_host::PerDevice<Occ> occ_cache;
+  Occ occ{};
+  int st = occ_cache.get(&occ, [&](Occ& v) -> int {
+    SLSP_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    v.smem = 0;
+    return SLSP_OK;
+  });
+  if (st) return st;
+  int per_sm = occ.per_sm;
+  if (occ.smem != smem) {  // rare (the row length changed): query and refresh this device's entry
+    SLSP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, smem));
     int dev = 0;
     SLSP_CUDA_TRY(cudaGetDevice(&dev));
-    SLSP_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    SLSP_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    std::lock_guard<std::mutex> g(occ_cache.mu);
+    occ_cache.val[dev] = Occ{smem, per_sm};
   }
-  if (cached_smem != smem) {
-    SLSP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cached_per_sm, k, kThreads, smem));
-    cached_smem = smem;
-  }
-  const int per_sm = cached_per_sm;
-  const int64_t cap = static_cast<int64_t>(sms) * (per_sm > 0 ? per_sm : 1);
+  const int64_t cap = static_cast<int64_t>(slsp_host::num_sms()) * (per_sm > 0 ? per_sm : 1);
   const unsigned grid = static_cast<unsigned>(a.rows < cap ? a.rows : cap);
   k<<<grid, kThreads, smem, s>>>(a);
   SLSP_LAUNCH_CHECK();

@@ -567,21 +567,22 @@ __global__ void load_compressed_kernel(const uint8_t* __restrict__ vals, const u
   }
 }
 
-// The byte-permute table lives in device memory (4 KB, uploaded once per
-// process; too large for a kernel parameter). Env SLSP_PACK_PATH=1 selects the
-// table-walk kernel (perf probing).
-const Lut8p* upload_lut8p(const Lut8& t) {
-  static Lut8p host = build_lut8p(t);
-  void* d = nullptr;
-  if (cudaMalloc(&d, sizeof(Lut8p)) != cudaSuccess) return nullptr;
-  if (cudaMemcpy(d, &host, sizeof(Lut8p), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
-  return static_cast<const Lut8p*>(d);
+// The byte-permute table lives in device memory (4 KB, too large for a
+// kernel parameter), uploaded once per device and kept for the process. Env
+// SLSP_PACK_PATH=1 selects the table-walk kernel (perf probing).
+int device_lut8p(const Lut8& t, const Lut8p** out) {
+  static const Lut8p host = build_lut8p(t);
+  static slsp_host::PerDevice<const Lut8p*> cache;
+  return cache.get(out, [](const Lut8p*& v) -> int {
+    void* d = nullptr;
+    SLSP_CUDA_TRY(cudaMalloc(&d, sizeof(Lut8p)));
+    SLSP_CUDA_TRY(cudaMemcpy(d, &host, sizeof(Lut8p), cudaMemcpyHostToDevice));
+    v = static_cast<const Lut8p*>(d);
+    return SLSP_OK;
+  });
 }
 
-int pack_path() {
-  const char* e = std::getenv("SLSP_PACK_PATH");
-  return e && *e ? e[0] - '0' : 2;
-}
+int pack_path() { return static_cast<int>(slsp_host::knob("SLSP_PACK_PATH", 2)); }
 
 template <int MODE>
 int launch_pack(int esz, PackArgs& a, cudaStream_t s) {
@@ -594,11 +595,14 @@ int launch_pack(int esz, PackArgs& a, cudaStream_t s) {
 #define SLSP_PACK_LAUNCH(E)                                                                  \
   do {                                                                                       \
     auto k = pack_kernel<E, MODE>;                                                           \
-    static bool attr_set = false;                                                            \
-    if (!attr_set) {                                                                         \
+    static slsp_host::PerDevice<int> attr_set; /* the smem opt-in is per device */           \
+    int ok_ = 0;                                                                             \
+    int st_ = attr_set.get(&ok_, [&](int& v) -> int {                                               \
       SLSP_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024)); \
-      attr_set = true;                                                                       \
-    }                                                                                        \
+      v = 1;                                                                                 \
+      return SLSP_OK;                                                                        \
+    });                                                                                      \
+    if (st_) return st_;                                                                     \
     k<<<grid, kThreads, smem, s>>>(a);                                                       \
   } while (0)
   switch (esz) {
@@ -684,8 +688,8 @@ int slsp_pack_compress(int dtype, const void* w, int64_t rows, int64_t cols, int
         if (pack_path() == 1) {
           pack68_kernel<1><<<grid, 256, 0, s>>>(in, rows, cols, z, dtype, lut, out, ld_vals, meta, ld_meta, status);
         } else {
-          static const Lut8p* dlut = upload_lut8p(lut);
-          if (!dlut) return SLSP_ERR_CUDA;
+          const Lut8p* dlut = nullptr;
+          if ((st = device_lut8p(lut, &dlut))) return st;
           pack68b_kernel<<<grid, 256, 0, s>>>(in, rows, cols, z, dtype, dlut, out, ld_vals, meta, ld_meta, status);
         }
       else

@@ -3,9 +3,66 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <atomic>
+#include <string>
+#include <utility>
+#include <vector>
+
 #include "internal.h"
 
+extern char** environ;
+
 namespace slsp_host {
+
+namespace {
+using KnobSnapshot = std::vector<std::pair<std::string, std::string>>;
+std::atomic<const KnobSnapshot*> g_knobs{nullptr};
+std::mutex g_knobs_mu;
+
+const KnobSnapshot* snapshot_knobs() {
+  auto* snap = new KnobSnapshot();
+  for (char** e = environ; e && *e; ++e) {
+    if (std::strncmp(*e, "SLSP_", 5) != 0) continue;
+    const char* eq = std::strchr(*e, '=');
+    if (eq) snap->emplace_back(std::string(*e, eq - *e), std::string(eq + 1));
+  }
+  return snap;
+}
+}  // namespace
+
+const char* knob_str(const char* name) {
+  const KnobSnapshot* k = g_knobs.load(std::memory_order_acquire);
+  if (!k) {
+    std::lock_guard<std::mutex> g(g_knobs_mu);
+    k = g_knobs.load(std::memory_order_acquire);
+    if (!k) {
+      k = snapshot_knobs();
+      g_knobs.store(k, std::memory_order_release);
+    }
+  }
+  for (const auto& kv : *k)
+    if (kv.first == name) return kv.second.c_str();
+  return nullptr;
+}
+
+int current_device(int* dev) {
+  SLSP_CUDA_TRY(cudaGetDevice(dev));
+  if (*dev < 0 || *dev >= kMaxDevices) return SLSP_ERR_UNSUPPORTED;
+  return SLSP_OK;
+}
+
+int num_sms() {
+  static PerDevice<int> cache;
+  int sms = 0;
+  if (cache.get(&sms, [](int& v) -> int {
+        int dev = 0;
+        SLSP_CUDA_TRY(cudaGetDevice(&dev));
+        SLSP_CUDA_TRY(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
+        return v > 0 ? SLSP_OK : SLSP_ERR_CUDA;
+      }))
+    return 0;
+  return sms;
+}
 
 static thread_local char g_last_cuda_error[256] = "";
 
@@ -48,18 +105,21 @@ int require_sm100() {
 }
 
 bool pdl_enabled() {  // off by default: measured 1% slower on the bench step
-  static const bool on = [] {
-    const char* e = std::getenv("SLSP_PDL");
-    return e && e[0] == '1';
-  }();
-  return on;
+  return knob("SLSP_PDL", 0) == 1;
 }
 
 }  // namespace slsp_host
 
 extern "C" {
 
-int slsp_version(void) { return 100; }
+int slsp_version(void) { return 200; }
+
+void slsp_reload_knobs(void) {
+  // The previous snapshot is leaked on purpose: a concurrent reader may still
+  // hold it (knobs are a probing aid, reloaded a handful of times per process).
+  std::lock_guard<std::mutex> g(slsp_host::g_knobs_mu);
+  slsp_host::g_knobs.store(slsp_host::snapshot_knobs(), std::memory_order_release);
+}
 
 const char* slsp_status_string(int status) {
   switch (status) {

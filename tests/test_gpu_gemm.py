@@ -200,8 +200,6 @@ def test_decode_split_k_int8_bit_exact(slsp, orc, m):
 def test_decode_split_k_bf16_epilogue_identical(slsp, m):
     """BF16 outputs of a split-K GEMM (workspace + finishing kernel) equal the
     unsplit GEMM's bit for bit (INT8: same int32 sums, same fp32 epilogue)."""
-    import os
-
     g = torch.Generator(device="cuda").manual_seed(m)
     n, k = 2048, 4096
     w = slsp.magnitude_prune(torch.randint(-127, 128, (n, k), dtype=torch.int8, device="cuda", generator=g), 6, 8)
@@ -212,13 +210,11 @@ def test_decode_split_k_bf16_epilogue_identical(slsp, m):
     q, q_s = slsp.quantize_rows(x)
     outs = {}
     for ks in ("1", "4"):  # forced unsplit, then a 4-way split
-        os.environ["SLSP_GEMM_KSPLIT"] = ks
-        try:
+        with slsp.knobs(SLSP_GEMM_KSPLIT=ks):
             for mode in (slsp.OUT_BF16_NM, slsp.OUT_BF16_MN):
+                assert slsp.sparse_gemm_config(pw, m, mode)["ksplit"] == int(ks)
                 outs[(ks, mode, "s")] = slsp.sparse_gemm(pw, payload, s_ch=s_ch, s_tok=s_tok, out_mode=mode)
                 outs[(ks, mode, "d")] = slsp.dense_gemm(w, q.view(torch.int8), s_ch=s_ch, s_tok=q_s, out_mode=mode)
-        finally:
-            del os.environ["SLSP_GEMM_KSPLIT"]
     torch.cuda.synchronize()
     for mode in (slsp.OUT_BF16_NM, slsp.OUT_BF16_MN):
         for kind in ("s", "d"):
@@ -251,11 +247,12 @@ def test_gpu_check_equivalence_rejects_noncompliant(slsp):
 
 @pytest.mark.parametrize("kind", ["int8", "fp8"])
 def test_half_k_stage_config_identical(slsp, kind):
-    """The half-k-stage tile config (SLSP_GEMM_KHALF: 64-byte A rows, one
-    metadata atom and two MMAs per stage) reproduces the default config's
-    BF16 output bit for bit (INT8: same exact sums; FP8: same MMA order)."""
-    import os
-
+    """The half-k-stage two-subtile config (SLSP_GEMM_KHALF: 64-byte A rows,
+    one metadata atom and two MMAs per stage and subtile) reproduces the
+    default two-subtile config's BF16 output bit for bit (INT8: same exact
+    sums; FP8: same MMA order). Both runs are forced onto two-subtile tiles
+    (SLSP_GEMM_MSUB=2) and the test asserts that the two launches really are
+    different configurations."""
     g = torch.Generator(device="cuda").manual_seed(11)
     n, k, m = 1536, 3584, 1000
     if kind == "int8":
@@ -269,18 +266,16 @@ def test_half_k_stage_config_identical(slsp, kind):
     s_ch = torch.rand(n, device="cuda", generator=g) * 0.01 + 0.001
     pw = slsp.pack_compress(w, 6, 8)
     payload, s_tok = slsp.fused_quant_slide(x, 6, 8, kind=qk)
-    outs = []
-    os.environ["SLSP_GEMM_BN256_MAXM"] = "0"  # keep M = 1000 on the two-subtile tiles half k-stages apply to
-    try:
-        for kh in ("0", "1"):
-            os.environ["SLSP_GEMM_KHALF"] = kh
-            try:
-                outs.append(slsp.sparse_gemm(pw, payload, s_ch=s_ch, s_tok=s_tok, out_mode=slsp.OUT_BF16_NM))
-            finally:
-                del os.environ["SLSP_GEMM_KHALF"]
-    finally:
-        del os.environ["SLSP_GEMM_BN256_MAXM"]
+    outs, cfgs = [], []
+    for kh in ("0", "1"):
+        # M = 1000 would take 256-token one-subtile tiles: keep it on the two-subtile ones
+        with slsp.knobs(SLSP_GEMM_BN256_MAXM=0, SLSP_GEMM_MSUB=2, SLSP_GEMM_KHALF=kh):
+            cfgs.append(slsp.sparse_gemm_config(pw, m, slsp.OUT_BF16_NM))
+            outs.append(slsp.sparse_gemm(pw, payload, s_ch=s_ch, s_tok=s_tok, out_mode=slsp.OUT_BF16_NM))
     torch.cuda.synchronize()
+    assert cfgs[0]["subtiles"] == cfgs[1]["subtiles"] == 2
+    assert (cfgs[0]["half_k_stages"], cfgs[1]["half_k_stages"]) == (0, 1)
+    assert cfgs[0]["stages"] < cfgs[1]["stages"]
     if kind == "int8":
         assert torch.equal(outs[0].view(torch.int16), outs[1].view(torch.int16))
     else:  # fp32 accumulation: the per-MMA k order is the same, so equal in practice; allow 1 bf16 ulp

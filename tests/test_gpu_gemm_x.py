@@ -6,7 +6,6 @@ in shared memory and the weights are in slsp_gemm_order's window order. The
 contract: int32 accumulators bit-exact vs the oracle's packed-word
 sparse_gemm (gemm.hpp:199-233) on fused_quant_slide's payload, and the BF16
 dequant epilogue bit-identical to slsp_sparse_gemm's."""
-import os
 
 import numpy as np
 import pytest
@@ -23,14 +22,9 @@ def dev(a):
 
 
 @pytest.fixture(params=["1", "2"], ids=["msub1", "msub2"])
-def msub(request):
-    old = os.environ.get("SLSP_GEMM_MSUB")
-    os.environ["SLSP_GEMM_MSUB"] = request.param
-    yield request.param
-    if old is None:
-        del os.environ["SLSP_GEMM_MSUB"]
-    else:
-        os.environ["SLSP_GEMM_MSUB"] = old
+def msub(request, slsp):
+    with slsp.knobs(SLSP_GEMM_MSUB=request.param):
+        yield request.param
 
 
 @pytest.mark.parametrize("n,k,m", [(256, 512, 224), (512, 1024, 448), (300, 1000, 250), (1024, 3584, 700),
