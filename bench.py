@@ -476,27 +476,24 @@ def run_e2e(slsp, torch, layers, xs, outs, out_mode, z, l, stream, device, args,
 
 # ---------------------------------------------------------- CPU baseline --
 # The reference's CPU path (oracle/_ref: its headers compiled unmodified; the
-# plain-C port when absent) needs ~8 min per Qwen2.5-7B layer at M = 8192, so
-# a step times a bounded sample and extrapolates: per layer, fused_quant_slide
-# (quantize.hpp:122-174, parallel over tokens) over T sampled tokens and the
-# packed-word sparse_gemm (gemm.hpp:199-233, parallel over weight rows) over R
-# sampled rows x the same T tokens, timed separately, then
-#     t_layer = t_lift * M / T + t_gemm * (N * M) / (R * T)
-# (both are linear in the sampled extent at >= 5 rows per thread). The GPU
-# arm also times the full o_proj layer once and reports the extrapolation's
-# error on it.
-def sample_rows(n: int, per: int = 16) -> list[int]:
-    """16-row groups spread over the weight rows: both CTAs of a pair and both
+# plain-C port when absent) needs minutes per full Qwen2.5-7B step at M = 8192,
+# so a step times a bounded sample and extrapolates: per layer,
+# fused_quant_slide (quantize.hpp:122-174, parallel over tokens) over all M
+# tokens and the packed-word sparse_gemm (gemm.hpp:199-233, parallel over
+# weight rows) over R = 288 sampled weight rows x all M tokens, timed
+# separately; the GEMM is linear in the rows (>= 18 rows per thread on 16
+# cores), so t_layer = t_lift + t_gemm * N / R. The GPU arm also times the
+# full o_proj layer once and reports the extrapolation's error on it.
+def sample_rows(n: int, per: int = 48) -> list[int]:
+    """48-row groups spread over the weight rows: both CTAs of a pair and both
     M-subtiles of the first 512-row tile, a middle group and the last rows."""
     starts = sorted({0, 128, 256, 384, (n // 2) // 128 * 128, max(0, n - per)})
     return sorted({r for s0 in starts for r in range(s0, min(n, s0 + per))})
 
 
 def sample_tokens(m: int) -> list[int]:
-    """The first two 224-token tiles, two in the middle, the last full tile
-    and the 128-token tail tile of M = 8192 (352 tokens)."""
-    mid = (m // 2) // 224 * 224
-    return sorted({t for t in [*range(0, 448), *range(mid, mid + 448), *range(max(0, m - 352), m)] if t < m})
+    """All tokens: every token tile, the 128-token tail tile of M = 8192 included."""
+    return list(range(m))
 
 
 def cpu_layer_times(R, vals, codes, x_bf16, z, l, threads):
@@ -512,6 +509,7 @@ def cpu_layer_times(R, vals, codes, x_bf16, z, l, threads):
 
 
 def extrapolate(t_lift, t_gemm, n, m, rows, toks):
+    """Full-layer time from the sample: lift linear in tokens, GEMM in rows x tokens."""
     return t_lift * m / toks + t_gemm * (n * m) / (rows * toks)
 
 
@@ -563,9 +561,9 @@ def cpu_baseline(slsp, torch, layers, xs, outs, out_mode, z, l):
                 "extrapolation_error": round(est / (tl + tg) - 1, 4)}
     total_flops = sum(L.flops for L in layers)
     baseline = {"value": round(total_flops / t_total / 1e12, 6), "unit": UNIT, "cores": threads, "kind": kind,
-                "sample": "per layer: fused_quant_slide over 1248 sampled tokens + packed-word sparse_gemm over "
-                          "~96 sampled weight rows x those tokens, timed separately and extrapolated to the full "
-                          f"layer (t_lift*M/T + t_gemm*N*M/(R*T)); {t_sample:.1f} s sampled on {threads} threads, "
+                "sample": "per layer: fused_quant_slide over all M tokens + packed-word sparse_gemm over 288 "
+                          "sampled weight rows x all M tokens, timed separately and extrapolated to the full layer "
+                          f"(t_lift + t_gemm*N/R); {t_sample:.1f} s sampled on {threads} threads, "
                           f"{t_total:.0f} s extrapolated per step",
                 "extrapolated_seconds_per_step": round(t_total, 1), "layers": per_layer, "full_o_proj": full}
     parity = {"bit_exact": mism == 0, "mismatches": mism, "outputs_checked": checked,
@@ -617,10 +615,10 @@ def run_reference(args, world, rank, local):
     dt = sum(ts) / len(ts)
     flops = sum(2.0 * m * n * k for _, n, k in WORKLOADS[args.workload])
     value = flops / dt / 1e12
-    sample = (f"per layer of {args.workload}: fused_quant_slide over {len(sample_tokens(m))} of {m} tokens + "
-              f"packed-word sparse_gemm over ~96 sampled weight rows x those tokens, timed separately and "
-              f"extrapolated to the full layer (t_lift*M/T + t_gemm*N*M/(R*T)); ms_per_step is the extrapolated "
-              f"full-step time")
+    sample = (f"per layer of {args.workload}: fused_quant_slide over all {m} tokens + packed-word sparse_gemm over "
+              f"288 sampled weight rows x all tokens, timed separately and extrapolated to the full layer "
+              f"(t_lift + t_gemm*N/R; validated against a full o_proj in the GPU arm's cpu_baseline); ms_per_step "
+              f"is the extrapolated full-step time")
     print(json.dumps({
         "metric": METRIC, "value": round(value, 6), "unit": UNIT, "impl": "reference", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True,

@@ -51,20 +51,29 @@ constexpr int epi_cols(int msub, int bn, int out) {
   return msub == 2 ? (out == SLSP_OUT_BF16_NM ? 32 : 16) : (out == SLSP_OUT_RAW_NM || bn % 64 != 0) ? 32 : 64;
 }
 
-template <bool SPARSE_, MmaKind KIND_, int BN_, int STAGES_, int OUT_, int MSUB_ = 1, int LIFT_ = 0, int KH_ = 0>
+template <bool SPARSE_, MmaKind KIND_, int BN_, int STAGES_, int OUT_, int MSUB_ = 1, int LIFT_ = 0, int KH_ = 0,
+          int NPAIR_ = 1>
 struct Cfg {
   static constexpr bool SPARSE = SPARSE_;
   static constexpr MmaKind KIND = KIND_;
   static constexpr int BN = BN_;          // tokens per pair tile (MMA N)
   static constexpr int OUT = OUT_;
-  static constexpr int CL = 2;            // one CTA pair per cluster
-  static constexpr int NPAIR = 1;
+  // Weight multicast: NPAIR CTA pairs per cluster run the SAME weight tile on
+  // NPAIR consecutive token tiles. Each weight subtile (A + metadata) of a
+  // stage is fetched from L2 once, by one pair, and TMA-multicast into the
+  // same ring slot of every pair (the rank-r CTAs of all pairs); activations
+  // stay per pair. L2->SM bytes per stage and pair drop from A+E+B to
+  // (A+E)/NPAIR+B; the pairs' rings run in lockstep (a slot is refilled once
+  // every pair's MMAs released it).
+  static constexpr int NPAIR = NPAIR_;
+  static constexpr int CL = 2 * NPAIR;    // CTAs per cluster
   // M-subtiles: the pair runs MSUB UMMAs (M=256 each) per k-step against the
   // same activation stage, so B traffic per MAC drops by MSUB. TMEM then holds
   // MSUB accumulators per tile; with MSUB=2 they are single-buffered and
   // 4*MSUB epilogue warps drain them in parallel.
   static constexpr int MSUB = MSUB_;
   static_assert(MSUB == 1 || MSUB == 2, "one or two M-subtiles per pair");
+  static_assert(NPAIR == 1 || (MSUB == 2 && NPAIR == 2), "weight multicast: two pairs, one subtile each");
   // In-SM lifting (sparse, (2N-2):2N with 8 | 2N... here 6:8): the activation
   // operand arrives UNLIFTED (quantized X, K bytes per token) and the lifted
   // K' is consumed in the GEMM window order of slsp_gemm_order: per 512
@@ -193,12 +202,14 @@ struct Params {
 // Raster: bands of `group` weight tiles; within a band the weight tile varies
 // fastest, so the clusters running concurrently share activation tiles (B)
 // and each band's weight tiles stay L2-resident while the band sweeps tokens.
-SLSP_DEVINL void tile_coords(int tile, const Params& p, int m_count, int& mt, int& nt, int& kb0, int& kb1) {
+// n_count: token super-tiles (NPAIR token tiles each).
+SLSP_DEVINL void tile_coords(int tile, const Params& p, int m_count, int n_count, int& mt, int& nt, int& kb0,
+                             int& kb1) {
   const int ks = tile % p.ksplit;  // split-K slice (innermost: the slices of a tile run concurrently)
   tile /= p.ksplit;
   kb0 = ks * p.num_kb / p.ksplit;
   kb1 = (ks + 1) * p.num_kb / p.ksplit;
-  const int per_group = p.group * p.n_tiles;
+  const int per_group = p.group * n_count;
   const int g = tile / per_group;
   const int first = g * p.group;
   const int gsize = min(p.group, m_count - first);
@@ -418,8 +429,11 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   const bool leader = rank == 0;
   const int cluster_id = blockIdx.x / C::CL;
   const int num_clusters = gridDim.x / C::CL;
-  const int m_super = (p.m_tiles + C::NPAIR - 1) / C::NPAIR;  // weight tiles per cluster step
-  const int num_tiles = m_super * p.n_tiles * p.ksplit;
+  // a cluster tile = one weight tile x NPAIR consecutive token tiles (pair p
+  // takes token tile ns * NPAIR + p; past the last one it recomputes token
+  // tile 0 — its loads stay in bounds — and stores nothing)
+  const int n_super = (p.n_tiles + C::NPAIR - 1) / C::NPAIR;
+  const int num_tiles = p.m_tiles * n_super * p.ksplit;
 
 #ifdef SLSP_WATCHDOG
   if (threadIdx.x == 0 && blockIdx.x < 2)
@@ -469,11 +483,16 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       // them (evict_last); weights stream through a raster band.
       const uint64_t pol_b = (p.hints & kHintBLast) ? policy_evict_last() : policy_evict_normal();
       const uint64_t pol_a = (p.hints & kHintAFirst) ? policy_evict_first() : policy_evict_normal();
+      // weight multicast: the rank-r CTA of every pair
+      uint16_t mc_mask = 0;
+#pragma unroll
+      for (int q = 0; q < C::NPAIR; ++q) mc_mask |= static_cast<uint16_t>(1u << (2 * q + rank));
       int it = 0;
       for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
-        int ms, nt, kb0, kb1;
-        tile_coords(tile, p, m_super, ms, nt, kb0, kb1);
-        int mt = ms * C::NPAIR + static_cast<int>(pair);
+        int mt, ns, kb0, kb1;
+        tile_coords(tile, p, p.m_tiles, n_super, mt, ns, kb0, kb1);
+        int nt = ns * C::NPAIR + static_cast<int>(pair);
+        if (nt >= p.n_tiles) nt = 0;  // idle pair of the last super-tile: in-bounds loads, no stores
         if (same) mt = nt = 0;
         long long wait_cycles = 0;
         const int a_row = mt * C::BM + static_cast<int>(rank) * C::A_ROWS;
@@ -511,9 +530,17 @@ __global__ void __launch_bounds__(C::THREADS, 1)
             const uint32_t bar = mapa_shared(smem_u32(&full[stage]), lead);
             const uint32_t bar1 = split ? mapa_shared(smem_u32(&full1[stage]), lead) : bar;
 #pragma unroll
-            for (int h = 0; h < C::MSUB; ++h)
-              tma_load_2d_cg2_hint(sA + stage * C::A_STAGE + h * C::A_SUB, &tmA, h ? bar1 : bar, kl * C::A_ROW,
-                                   a_row + h * 256, pol_a);
+            for (int h = 0; h < C::MSUB; ++h) {
+              if constexpr (C::NPAIR == 1) {
+                tma_load_2d_cg2_hint(sA + stage * C::A_STAGE + h * C::A_SUB, &tmA, h ? bar1 : bar, kl * C::A_ROW,
+                                     a_row + h * 256, pol_a);
+              } else if (h % C::NPAIR == static_cast<int>(pair)) {
+                // subtile h: fetched once by pair h, multicast to the rank-r CTA of every pair;
+                // each destination reports the bytes to its own pair leader's barrier
+                tma_load_2d_cg2_mc(sA + stage * C::A_STAGE + h * C::A_SUB, &tmA, h ? bar1 : bar, kl * C::A_ROW,
+                                   a_row + h * 256, mc_mask, pol_a);
+              }
+            }
             if constexpr (C::LIFT) {
               // X block j of period q: source bytes [512q + 256j, +256) into this CTA (local barrier)
               // xfull completes once per ring lap (slots alternate between X
@@ -538,9 +565,14 @@ __global__ void __launch_bounds__(C::THREADS, 1)
             if constexpr (C::SPARSE)  // one contiguous 4 KB tiled-metadata block per stage and subtile
               if (!skip_e)
 #pragma unroll
-                for (int h = 0; h < C::MSUB; ++h)
-                  tma_load_2d_cg2_hint(sE + stage * C::E_STAGE + h * C::E_SUB, &tmE, h ? bar1 : bar, 0,
-                                       (((a_row + h * 256) >> 7) * p.num_kb + kl) * 8 * C::E_ATOMS, pol_a);
+                for (int h = 0; h < C::MSUB; ++h) {
+                  const int erow = (((a_row + h * 256) >> 7) * p.num_kb + kl) * 8 * C::E_ATOMS;
+                  if constexpr (C::NPAIR == 1)
+                    tma_load_2d_cg2_hint(sE + stage * C::E_STAGE + h * C::E_SUB, &tmE, h ? bar1 : bar, 0, erow, pol_a);
+                  else if (h % C::NPAIR == static_cast<int>(pair))
+                    tma_load_2d_cg2_mc(sE + stage * C::E_STAGE + h * C::E_SUB, &tmE, h ? bar1 : bar, 0, erow, mc_mask,
+                                       pol_a);
+                }
           }
           if (++stage == C::STAGES) {
             stage = 0;
@@ -558,8 +590,8 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       int it = 0;
       const uint16_t all_ctas = static_cast<uint16_t>((1u << C::CL) - 1);
       for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
-        int ms_, nt_, kb0, kb1;
-        tile_coords(tile, p, m_super, ms_, nt_, kb0, kb1);
+        int mt_, ns_, kb0, kb1;
+        tile_coords(tile, p, p.m_tiles, n_super, mt_, ns_, kb0, kb1);
         const int acc = C::ACC_STAGES == 2 ? (it & 1) : 0;
         const uint32_t acc_phase = C::ACC_STAGES == 2 ? ((it >> 1) & 1) : (it & 1);
         // MSUB=1: double-buffered accumulators, tempty[acc]. MSUB=2: one
@@ -760,9 +792,9 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     const int nch = ncols / 16;
     int it = 0;
     for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
-      int ms, nt, kb0_, kb1_;
-      tile_coords(tile, p, m_super, ms, nt, kb0_, kb1_);
-      const int mt = ms * C::NPAIR + static_cast<int>(pair);
+      int mt, ns, kb0_, kb1_;
+      tile_coords(tile, p, p.m_tiles, n_super, mt, ns, kb0_, kb1_);
+      const int nt = ns * C::NPAIR + static_cast<int>(pair);  // >= n_tiles: idle pair, tcol0 >= m stores nothing
       const int64_t tcol0 = static_cast<int64_t>(nt) * C::BN + half * C::H0;
       const int64_t rowq = static_cast<int64_t>(mt) * C::BM + rank * C::A_ROWS + quarter * 32;  // lane 0's row
       const int64_t row0 = rowq + lane;
@@ -856,9 +888,9 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     int buf = 0;
     int it = 0;
     for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
-      int ms, nt, kb0_, kb1_;
-      tile_coords(tile, p, m_super, ms, nt, kb0_, kb1_);
-      const int mt = ms * C::NPAIR + static_cast<int>(pair);
+      int mt, ns, kb0_, kb1_;
+      tile_coords(tile, p, p.m_tiles, n_super, mt, ns, kb0_, kb1_);
+      const int nt = ns * C::NPAIR + static_cast<int>(pair);  // >= n_tiles: idle pair, t0 >= m stores nothing
       const int acc = C::ACC_STAGES == 2 ? (it & 1) : 0;
       const uint32_t acc_phase = C::ACC_STAGES == 2 ? ((it >> 1) & 1) : (it & 1);
       mbar_wait(&tfull[acc], acc_phase);
@@ -1118,7 +1150,7 @@ int run(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const 
   if (st) return st;
   p.m_tiles = static_cast<int>((p.n + C::BM - 1) / C::BM);
   p.n_tiles = static_cast<int>((p.m + C::BN - 1) / C::BN);
-  int tiles = (p.m_tiles + C::NPAIR - 1) / C::NPAIR * p.n_tiles;
+  int tiles = p.m_tiles * ((p.n_tiles + C::NPAIR - 1) / C::NPAIR);
   int clusters = max_clusters;
   const int cluster_cap = static_cast<int>(env_knob("SLSP_GEMM_CLUSTERS", 0));  // perf probing
   if (cluster_cap > 0 && clusters > cluster_cap) clusters = cluster_cap;
@@ -1158,28 +1190,35 @@ int run(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const 
   return SLSP_OK;
 }
 
-template <bool SPARSE, MmaKind K, int BN, int MSUB, int LIFT, int KH>
+template <bool SPARSE, MmaKind K, int BN, int MSUB, int LIFT, int KH, int NPAIR = 1>
 int run_out_cl(int out_mode, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const CUtensorMap& o,
                const Params& p, cudaStream_t s, slsp_gemm_config* q) {
   switch (out_mode) {  // STAGES = 0: as many as fit
-    case SLSP_OUT_RAW_NM: return run<Cfg<SPARSE, K, BN, 0, SLSP_OUT_RAW_NM, MSUB, LIFT, KH>>(a, b, e, o, p, s, q);
-    case SLSP_OUT_BF16_NM: return run<Cfg<SPARSE, K, BN, 0, SLSP_OUT_BF16_NM, MSUB, LIFT, KH>>(a, b, e, o, p, s, q);
-    case SLSP_OUT_BF16_MN: return run<Cfg<SPARSE, K, BN, 0, SLSP_OUT_BF16_MN, MSUB, LIFT, KH>>(a, b, e, o, p, s, q);
+    case SLSP_OUT_RAW_NM:
+      return run<Cfg<SPARSE, K, BN, 0, SLSP_OUT_RAW_NM, MSUB, LIFT, KH, NPAIR>>(a, b, e, o, p, s, q);
+    case SLSP_OUT_BF16_NM:
+      return run<Cfg<SPARSE, K, BN, 0, SLSP_OUT_BF16_NM, MSUB, LIFT, KH, NPAIR>>(a, b, e, o, p, s, q);
+    case SLSP_OUT_BF16_MN:
+      return run<Cfg<SPARSE, K, BN, 0, SLSP_OUT_BF16_MN, MSUB, LIFT, KH, NPAIR>>(a, b, e, o, p, s, q);
   }
   return SLSP_ERR_INVALID;
 }
 
 // Tile shape: 1 or 2 M-subtiles per CTA pair (env SLSP_GEMM_MSUB for the
-// sparse kernel, SLSP_DGEMM_MSUB for the dense one; decode tiles: 1).
+// sparse kernel, SLSP_DGEMM_MSUB for the dense one; decode tiles: 1), and
+// for two-subtile 8-bit sparse tiles optionally two pairs per cluster sharing
+// the weight tile by multicast (npair = 2).
 template <bool SPARSE, MmaKind K, int BN, int LIFT = 0>
 int run_out(int out_mode, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const CUtensorMap& o,
-            const Params& p, cudaStream_t s, uint32_t msub, uint32_t kh, slsp_gemm_config* q) {
+            const Params& p, cudaStream_t s, uint32_t msub, uint32_t kh, slsp_gemm_config* q, uint32_t npair = 1) {
   constexpr bool two_sub = BN >= 128 && !(SPARSE && BN > 224);  // two accumulators fit TMEM
   if constexpr (BN >= 128 && SPARSE && !LIFT && K != MmaKind::F16) {
     if (kh && msub == 1) return run_out_cl<SPARSE, K, BN, 1, 0, 1>(out_mode, a, b, e, o, p, s, q);
-    if constexpr (two_sub)
+    if constexpr (two_sub) {
       if (kh && msub == 2 && out_mode == SLSP_OUT_BF16_NM)
         return run_out_cl<SPARSE, K, BN, 2, 0, 1>(out_mode, a, b, e, o, p, s, q);
+      if (!kh && msub == 2 && npair == 2) return run_out_cl<SPARSE, K, BN, 2, 0, 0, 2>(out_mode, a, b, e, o, p, s, q);
+    }
   }
   if constexpr (two_sub)
     if (msub == 2) return run_out_cl<SPARSE, K, BN, 2, LIFT, 0>(out_mode, a, b, e, o, p, s, q);
@@ -1220,6 +1259,7 @@ constexpr int kSparseBN256 = 256;
 // bit-identical; at M = 8192 one-subtile tiles lose 10-20% with them
 constexpr uint32_t kSparseKHalf1 = 1;
 constexpr uint32_t kDenseMsub = 1;
+constexpr uint32_t kSparseMc = 1;  // two pairs sharing the weight tile (two-subtile 8-bit tiles)
 constexpr uint32_t kRasterGroup = 16;  // measured best of {4, 8, 16, 32, 148} on Qwen2.5-7B shapes
 
 // M-subtiles for the sparse kernel: two subtiles (512 weight rows per pair,
@@ -1339,9 +1379,11 @@ int sparse_entry(int dtype, const void* values, const uint8_t* meta, int64_t n, 
     if (dtype == SLSP_DT_BF16)
       return run_out<true, MmaKind::F16, kSparseBN>(out_mode, ta, tb, te, to, p, s, msub, 0, q);
   }
+  // weight multicast across two pairs (env SLSP_GEMM_MC: 1 = off, 2 = on)
+  const uint32_t npair = !LIFT && msub == 2 && !kh && env_knob("SLSP_GEMM_MC", kSparseMc) == 2 ? 2u : 1u;
   if (dtype == SLSP_DT_I8)
-    return run_out<true, MmaKind::I8, kSparseBN, L>(out_mode, ta, tb, te, to, p, s, msub, kh, q);
-  return run_out<true, MmaKind::F8, kSparseBN, L>(out_mode, ta, tb, te, to, p, s, msub, kh, q);
+    return run_out<true, MmaKind::I8, kSparseBN, L>(out_mode, ta, tb, te, to, p, s, msub, kh, q, npair);
+  return run_out<true, MmaKind::F8, kSparseBN, L>(out_mode, ta, tb, te, to, p, s, msub, kh, q, npair);
 }
 
 int dense_entry(int dtype, const void* w, int64_t n, int64_t k, const void* act, int64_t m, const float* s_ch,

@@ -44,6 +44,7 @@ for k in [int(v) for v in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["35
     ref = {}
     for path in ("2", "1"):
         os.environ["SLSP_LIFT_ROW"] = path
+        slsp.reload_knobs()
         t_l = burst(lambda: slsp.fused_quant_slide(x, 6, 8, check=False, payload=pay, scales=sc))
         p1 = pay.clone()
         t_q = burst(lambda: slsp.quantize_rows(x, check=False, out=q, scales=sc))

@@ -22,6 +22,7 @@ for dt in ("int8", "e4m3"):
     ref = None
     for path in ("1", "2"):
         os.environ["SLSP_PACK_PATH"] = path
+        slsp.reload_knobs()
         pw = slsp.pack_compress(w, 6, 8, check=False)
         ts = []
         for _ in range(15):

@@ -1,7 +1,7 @@
 """GEMM config sweep in ONE process (GPU box; perf probing, not a test).
 
-Env knobs are read per call by the library, so each config is applied by
-setting os.environ before capturing a CUDA graph of `reps` launches. Prints one
+Each config is applied by setting os.environ + slsp.reload_knobs() before
+capturing a CUDA graph of `reps` launches. Prints one
 line per (kernel, config, layer): ms per launch (median of `rounds` graph
 replays, CUDA events) and effective TFLOPS; sparse/dense ratios at the end.
 
@@ -41,6 +41,7 @@ def apply(kv, dense):
     for k, v in kv.items():
         pre = "SLSP_DGEMM_" if dense and k in DENSE_KEYS else "SLSP_GEMM_"
         os.environ[pre + k] = v
+    slsp.reload_knobs()  # the library snapshots SLSP_* knobs
 
 
 class Clocks:

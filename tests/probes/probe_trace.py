@@ -56,9 +56,11 @@ print(f"{kind} msub={os.environ.get('SLSP_GEMM_MSUB', '1')} dbg={os.environ.get(
 
 trace = torch.zeros(65536 + 16 * 256 * 2, dtype=torch.int64, device=dev)
 os.environ["SLSP_GEMM_TRACE"] = str(trace.data_ptr())
+slsp.reload_knobs()
 run()
 torch.cuda.synchronize()
 del os.environ["SLSP_GEMM_TRACE"]
+slsp.reload_knobs()
 t = trace[:65536].view(-1, 16).cpu()
 st = trace[65536:].view(16, 256, 2).cpu()
 n = int((t[:, 0] != 0).sum())
