@@ -131,6 +131,13 @@ SLSP_DEVINL void tma_prefetch(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
 
+// L2 prefetch of one tensor box (no shared-memory destination, no completion).
+SLSP_DEVINL void tma_prefetch_l2_2d(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
+
 // 2-CTA (cta_group::2) tensor loads: data lands in the issuing CTA's smem,
 // completion bytes are reported to `bar_cluster` (the leader CTA's barrier).
 SLSP_DEVINL void tma_load_2d_cg2(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,

@@ -188,6 +188,9 @@ struct Params {
   // the normal epilogue.
   int splitbar;  // SPLIT configs: per-subtile full barriers (env SLSP_GEMM_SPLITBAR, default 1)
   int ksplit;
+  int pf_stages;  // L2-prefetch the next tile's first pf_stages k-blocks (env SLSP_GEMM_PF)
+  int pf_at;      // ... when this tile's k-block pf_at is issued (env SLSP_GEMM_PFAT)
+  int pace_ns;   // REG epilogue: sleep between output boxes (env SLSP_GEMM_PACE, perf probing)
   void* ws;
   int64_t ws_cap;  // workspace bytes (bounds ksplit)
 };
@@ -499,6 +502,28 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         const int b_row = nt * C::BN + static_cast<int>(rank) * C::B_ROWS;
         for (int kb = kb0; kb < kb1; ++kb) {
           const int kl = same ? 0 : kb;
+          if (p.pf_stages && kb == kb0 + p.pf_at && tile + num_clusters < num_tiles) {
+            // warm L2 with the next tile's first k-blocks: at a tile start the
+            // ring's first stages are new weight / token tiles whose loads miss
+            int mt2, ns2, kc0, kc1;
+            tile_coords(tile + num_clusters, p, p.m_tiles, n_super, mt2, ns2, kc0, kc1);
+            int nt2 = ns2 * C::NPAIR + static_cast<int>(pair);
+            if (nt2 >= p.n_tiles) nt2 = 0;
+            const int a2 = mt2 * C::BM + static_cast<int>(rank) * C::A_ROWS;
+            const int b2 = nt2 * C::BN + static_cast<int>(rank) * C::B_ROWS;
+            const int kend = min(kc1, kc0 + p.pf_stages);
+            for (int k2 = kc0; k2 < kend; ++k2) {
+#pragma unroll
+              for (int h = 0; h < C::MSUB; ++h) {
+                tma_prefetch_l2_2d(&tmA, k2 * C::A_ROW, a2 + h * 256);
+                if constexpr (C::SPARSE)
+                  tma_prefetch_l2_2d(&tmE, 0, (((a2 + h * 256) >> 7) * p.num_kb + k2) * 8 * C::E_ATOMS);
+              }
+              if constexpr (!C::LIFT)
+#pragma unroll
+                for (int at = 0; at < C::B_ATOMS; ++at) tma_prefetch_l2_2d(&tmB, k2 * C::K_BYTES_B + at * 128, b2);
+            }
+          }
           if (p.trace) {
             const long long t0 = clock64();
             mbar_wait(&empty[stage], phase ^ 1);
@@ -602,6 +627,11 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         SLSP_TRACE(it, 0);
+        if (p.trace && blockIdx.x == 0) {  // wall clock beside clock64: the SM clock the tile ran at
+          unsigned long long gt;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+          p.trace[it * 16 + 10] = gt;
+        }
         const uint32_t d_tmem = tmem + acc * C::MSUB * C::ACC_COLS;
         // subtile h's metadata copy + 4 MMAs for k-block kb held in ring stage st
         const bool no_mma = p.debug & kDbgNoMma;
@@ -836,6 +866,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
           for (int b = 0; b < NCH / 2; ++b) {
             const int64_t t0 = tcol0 + 32 * b;
             if (2 * b >= nch || t0 >= p.m) break;  // warp-uniform
+            if (p.pace_ns && (h || b)) __nanosleep(p.pace_ns);
             if (lane == 0) bulk_wait_read<0>();  // staging buffer read by the previous box's store
             __syncwarp();
             // [32 rows][64 B] staging in the map's 64-byte swizzle (16-byte chunk ^= (row >> 1) & 3)
@@ -1361,6 +1392,9 @@ int sparse_entry(int dtype, const void* values, const uint8_t* meta, int64_t n, 
   p.hints = env_knob("SLSP_GEMM_HINTS", kDefaultHints);
   p.group = static_cast<int>(env_knob("SLSP_GEMM_GROUP", kRasterGroup));
   p.splitbar = static_cast<int>(env_knob("SLSP_GEMM_SPLITBAR", 1));
+  p.pace_ns = static_cast<int>(env_knob("SLSP_GEMM_PACE", 0));
+  p.pf_stages = static_cast<int>(env_knob("SLSP_GEMM_PF", 0));
+  p.pf_at = static_cast<int>(env_knob("SLSP_GEMM_PFAT", 8));
   constexpr int L = LIFT ? 1 : 0;
   if constexpr (!LIFT) {
     if (decode) {

@@ -22,7 +22,9 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
 import paper_2603_05232_b200 as slsp  # noqa: E402
 
 SHAPES = {"qkv": (4608, 3584), "o": (3584, 3584), "gate_up": (37888, 3584), "down": (3584, 18944),
-          "cfg1": (4096, 4096)}  # BASELINE config 1 (K = N = 4096)
+          "cfg1": (4096, 4096),
+          # L2-residency probes: gate_up's K with fewer weight rows (operands fit in L2)
+          "gu4k": (4096, 3584), "gu8k": (8192, 3584), "gu16k": (16384, 3584)}  # BASELINE config 1 (K = N = 4096)
 DENSE_KEYS = {"CLUSTER", "MSUB", "DECODE_M"}
 
 

@@ -78,6 +78,14 @@ for i in range(min(n, show)):
 if n > 2:
     tot = int(t[n - 1, 2]) - t0
     print(f"avg cycles/tile {tot / (n - 1):.0f}")
+    # SM clock while the tiles ran: clock64 vs %globaltimer (ns) at the tile starts
+    dc = int(t[n - 1, 0]) - t0
+    dt = int(t[n - 1, 10]) - int(t[0, 10])
+    if dt > 0:
+        q1 = max(1, (n - 1) // 4)
+        mhz = [(int(t[j + q1, 0]) - int(t[j, 0])) / max(1, int(t[j + q1, 10]) - int(t[j, 10])) * 1e3
+               for j in range(0, n - 1 - q1 + 1, q1)]
+        print(f"SM clock over the tiles: {dc / dt * 1e3:.0f} MHz (per quarter: {', '.join(f'{v:.0f}' for v in mhz)})")
 
 # per-stage load latency: producer issue -> MMA sees the stage full
 import statistics  # noqa: E402
