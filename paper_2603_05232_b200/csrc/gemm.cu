@@ -187,6 +187,13 @@ struct Params {
   // (deterministic; exact for int32) and applies the epilogue. ksplit == 1:
   // the normal epilogue.
   int splitbar;  // SPLIT configs: per-subtile full barriers (env SLSP_GEMM_SPLITBAR, default 1)
+  // MSUB=2: issue subtile 0's MMAs of the last `tail0` k-blocks of a tile
+  // before subtile 1's and commit them to their own barrier (tfull[1]), so the
+  // epilogue drains subtile 0 while subtile 1 finishes and the next tile's
+  // subtile-0 MMAs start sooner (env SLSP_GEMM_TAIL0: 0 = one commit per tile
+  // after both subtiles, 1 = early subtile-0 commit only, 2 = + last two
+  // k-blocks reordered)
+  int tail0;
   int ksplit;
   int pf_stages;  // L2-prefetch the next tile's first pf_stages k-blocks (env SLSP_GEMM_PF)
   int pf_at;      // ... when this tile's k-block pf_at is issued (env SLSP_GEMM_PFAT)
@@ -676,6 +683,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
             tc_fence_after();
           }
         };
+        const uint16_t pair_epi = static_cast<uint16_t>(0x3u << lead);  // this pair's epilogues
         for (int kb = kb0; kb < kb1; ++kb) {
           if (p.trace) {
             const long long t0 = clock64();
@@ -687,7 +695,39 @@ __global__ void __launch_bounds__(C::THREADS, 1)
             mbar_wait(&full[stage], phase);
           }
           tc_fence_after();
+          if constexpr (C::MSUB == 2) {
+            if (p.tail0 == 2 && sub1_ready && kb == kb1 - 2) {
+              // last two k-blocks: sub0(k-1), sub0(k) | commit sub0 | sub1(k-1), sub1(k)
+              int st2 = stage + 1;
+              uint32_t ph2 = phase;
+              if (st2 == C::STAGES) {
+                st2 = 0;
+                ph2 ^= 1u;
+              }
+              issue(0, stage, kb);
+              mbar_wait(&full[st2], ph2);
+              tc_fence_after();
+              issue(0, st2, kb + 1);
+              tc_commit_mc(&tfull[1], pair_epi);
+              wait_full1(stage, phase);
+              issue(1, stage, kb);
+              tc_commit_mc(&empty[stage], all_ctas);
+              wait_full1(st2, ph2);
+              issue(1, st2, kb + 1);
+              tc_commit_mc(&empty[st2], all_ctas);
+              stage = st2 + 1;
+              phase = ph2;
+              if (stage == C::STAGES) {
+                stage = 0;
+                phase ^= 1u;
+              }
+              ++kb;
+              continue;
+            }
+          }
           issue(0, stage, kb);
+          // subtile 0 complete for this tile: its own commit (tfull[1]) ahead of subtile 1's last MMAs
+          if (C::MSUB == 2 && p.tail0 && kb == kb1 - 1) tc_commit_mc(&tfull[1], pair_epi);
           if constexpr (C::MSUB == 1) {
             tc_commit_mc(&empty[stage], all_ctas);  // every CTA of the cluster
           } else if (sub1_ready) {
@@ -728,7 +768,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         }
         SLSP_TRACE(it, 2);
         if (p.trace && blockIdx.x == 0) p.trace[it * 16 + 8] = wait_cycles;
-        tc_commit_mc(&tfull[acc], static_cast<uint16_t>(0x3u << lead));  // this pair's epilogues
+        tc_commit_mc(&tfull[acc], pair_epi);
       }
     }
   } else if (C::LIFT && warp >= 2 + C::EPI_WARPS) {
@@ -833,7 +873,8 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       for (int i = static_cast<int>(lane); i < ncols; i += 32)
         stok_sm[i] = tcol0 + i < p.m ? __ldg(p.s_tok + tcol0 + i) : 0.f;
       __syncwarp();
-      mbar_wait(&tfull[0], it & 1);
+      // subtile 0 is committed on its own barrier (tfull[1]) when p.tail0
+      mbar_wait(&tfull[p.tail0 ? 1 : 0], it & 1);
       tc_fence_after();
       if (warp == 2 && lane == 0) SLSP_TRACE(it, 3);
 
@@ -903,6 +944,10 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       };
       uint32_t pk0[NCH][8], pk1[NCH][8];
       drain(0, sc0, pk0);
+      if (p.tail0) {
+        mbar_wait(&tfull[0], it & 1);
+        tc_fence_after();
+      }
       drain(1, sc1, pk1);
       store(0, pk0);
       if (warp == 2 && lane == 0) SLSP_TRACE(it, 5);
@@ -924,12 +969,18 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       const int nt = ns * C::NPAIR + static_cast<int>(pair);  // >= n_tiles: idle pair, t0 >= m stores nothing
       const int acc = C::ACC_STAGES == 2 ? (it & 1) : 0;
       const uint32_t acc_phase = C::ACC_STAGES == 2 ? ((it >> 1) & 1) : (it & 1);
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
       // MSUB=2: all 8 warps drain subtile 0 (two warps per lane quarter,
-      // alternating chunks), release it, then subtile 1.
+      // alternating chunks), release it, then subtile 1; with p.tail0
+      // subtile 0 has its own barrier (tfull[1]), tfull[0] covers both
 #pragma unroll 1
       for (int h = 0; h < C::MSUB; ++h) {
+        if (C::MSUB == 2 && p.tail0) {
+          mbar_wait(&tfull[h == 0 ? 1 : 0], acc_phase);
+          tc_fence_after();
+        } else if (h == 0) {
+          mbar_wait(&tfull[acc], acc_phase);
+          tc_fence_after();
+        }
         const int64_t row0 = static_cast<int64_t>(mt) * C::BM + h * 256 + rank * C::A_ROWS + quarter * 32;
         float sc = 0.f;
         if constexpr (C::OUT != SLSP_OUT_RAW_NM) sc = (row0 + lane < p.n) ? __ldg(p.s_ch + row0 + lane) : 0.f;
@@ -1290,6 +1341,7 @@ constexpr int kSparseBN256 = 256;
 // bit-identical; at M = 8192 one-subtile tiles lose 10-20% with them
 constexpr uint32_t kSparseKHalf1 = 1;
 constexpr uint32_t kDenseMsub = 1;
+constexpr uint32_t kTail0 = 1;     // early subtile-0 commit (Params::tail0; 2 = + reorder, measured slower)
 constexpr uint32_t kSparseMc = 1;  // two pairs sharing the weight tile (two-subtile 8-bit tiles)
 constexpr uint32_t kRasterGroup = 16;  // measured best of {4, 8, 16, 32, 148} on Qwen2.5-7B shapes
 
@@ -1392,6 +1444,7 @@ int sparse_entry(int dtype, const void* values, const uint8_t* meta, int64_t n, 
   p.hints = env_knob("SLSP_GEMM_HINTS", kDefaultHints);
   p.group = static_cast<int>(env_knob("SLSP_GEMM_GROUP", kRasterGroup));
   p.splitbar = static_cast<int>(env_knob("SLSP_GEMM_SPLITBAR", 1));
+  p.tail0 = static_cast<int>(env_knob("SLSP_GEMM_TAIL0", kTail0));
   p.pace_ns = static_cast<int>(env_knob("SLSP_GEMM_PACE", 0));
   p.pf_stages = static_cast<int>(env_knob("SLSP_GEMM_PF", 0));
   p.pf_at = static_cast<int>(env_knob("SLSP_GEMM_PFAT", 8));

@@ -82,6 +82,7 @@ def main():
     ap.add_argument("--layers", default="gate_up")
     ap.add_argument("--sparse", default="MSUB=2")
     ap.add_argument("--dense", default="CLUSTER=2")
+    ap.add_argument("--sparsex", default="", help="configs of the in-SM-lifting kernel (sparse_gemm_x)")
     ap.add_argument("--seconds", type=float, default=1.5)
     ap.add_argument("--m", type=int, default=8192)
     args = ap.parse_args()
@@ -105,6 +106,14 @@ def main():
             apply(kv, False)
             run(nv, h, f"sparse {layer} {kv}", lambda: slsp.sparse_gemm(pw, payload, s_ch=s_ch, s_tok=s_tok,
                                                                          out_mode=slsp.OUT_BF16_NM, out=out),
+                ops, args.seconds)
+        if args.sparsex:
+            xq, _ = slsp.quantize_rows(x, kpad=slsp.round_up(k, 512))
+            pwx = pw.gemm_order()
+        for kv in parse_cfgs(args.sparsex) if args.sparsex else []:
+            apply(kv, False)
+            run(nv, h, f"sparsex {layer} {kv}", lambda: slsp.sparse_gemm_x(pwx, xq, s_ch=s_ch, s_tok=s_tok,
+                                                                            out_mode=slsp.OUT_BF16_NM, out=out),
                 ops, args.seconds)
         for kv in parse_cfgs(args.dense) if args.dense else []:
             apply(kv, True)
