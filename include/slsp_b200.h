@@ -168,6 +168,25 @@ SLSP_API int slsp_sparse_gemm(int dtype, const void* values, const uint8_t* meta
                      int64_t m, const float* s_ch, const float* s_tok, int out_mode, void* out, int64_t ldo,
                      slsp_stream_t stream);
 
+/* §8f #3 — the next layer's lift fused upstream. slsp_sparse_gemm with BF16
+ * outputs that also writes tok_amax[t] = max over this call's n output
+ * features of |y[t][.]| (the BF16-rounded outputs; zeroed first, then
+ * max-accumulated with atomics; NaN wins over Inf). Feeding y and tok_amax
+ * to slsp_fused_quant_slide_scaled gives exactly slsp_fused_quant_slide(y)
+ * (quantize.hpp:122-174) without its |x|max pass. No split-K. */
+SLSP_API int slsp_sparse_gemm_amax(int dtype, const void* values, const uint8_t* meta, int64_t n, int64_t kp,
+                                   const void* act, int64_t m, const float* s_ch, const float* s_tok, int out_mode,
+                                   void* out, int64_t ldo, float* tok_amax, slsp_stream_t stream);
+
+/* fused_quant_slide (quantize.hpp:122-174) given each row's |x|max
+ * (tok_amax, e.g. from slsp_sparse_gemm_amax): r = qmax/absmax, scale =
+ * float(absmax/qmax) in double exactly as the reference; a non-finite
+ * tok_amax[row] reports SLSP_ERR_NON_FINITE for that row like the
+ * unscaled entry. Same layouts and requirements as slsp_fused_quant_slide. */
+SLSP_API int slsp_fused_quant_slide_scaled(int in_dtype, const void* x, int64_t rows, int64_t cols, int z, int l,
+                                           int kind, int64_t kp, const float* tok_amax, uint32_t* payload,
+                                           float* scales, void* status_ws, int64_t* bad_row, slsp_stream_t stream);
+
 /* SLSP kind-2 container payload -> MMA-ready weights (
  * container.hpp:379-390 to_container / :424-435 compressed_from). values:
  * the container's values section on the device (rows x windows x 2 elements);

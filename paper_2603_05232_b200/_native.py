@@ -123,6 +123,9 @@ def lib() -> C.CDLL:
                 "slsp_load_compressed": (i32, [i32, vp, vp, i64, i64, i64, vp, vp, vp]),
                 "slsp_gemm_order": (i32, [i32, vp, vp, i64, i64, i64, vp, vp, i64, vp]),
                 "slsp_sparse_gemm_x": (i32, [i32, vp, vp, i64, i64, vp, i64, vp, vp, i32, vp, i64, vp]),
+                "slsp_sparse_gemm_amax": (i32, [i32, vp, vp, i64, i64, vp, i64, vp, vp, i32, vp, i64, vp, vp]),
+                "slsp_fused_quant_slide_scaled": (i32, [i32, vp, i64, i64, i32, i32, i32, i64, vp, vp, vp, vp, vp,
+                                                        vp]),
                 "slsp_tiled_meta_bytes": (i64, [i64, i64]),
                 "slsp_reload_knobs": (None, []),
                 "slsp_sparse_gemm_config": (i32, [i32, i64, i64, i64, i32, i64, C.POINTER(GemmConfig)]),
@@ -382,9 +385,15 @@ def _in_dtype(x: torch.Tensor) -> int:
 
 def fused_quant_slide(x: torch.Tensor, z: int, l: int, kind: int = QUANT_INT8, kp: int | None = None,
                       check: bool = True, payload: torch.Tensor | None = None,
-                      scales: torch.Tensor | None = None) -> tuple[torch.Tensor, torch.Tensor]:
-    """quantize.hpp:122-174 -> (payload rows x kp/4 uint32 words as int32 storage, scales fp32)."""
-    _require_cuda(x)
+                      scales: torch.Tensor | None = None,
+                      absmax: torch.Tensor | None = None) -> tuple[torch.Tensor, torch.Tensor]:
+    """quantize.hpp:122-174 -> (payload rows x kp/4 uint32 words as int32 storage, scales fp32).
+
+    absmax (fp32, one per row): each row's |x|max computed upstream — the
+    tok_amax of sparse_gemm(..., tok_amax=...) on the layer that produced x
+    (SURVEY §8f #3); the kernel then skips its own |x|max pass. The result is
+    identical to the call without it."""
+    _require_cuda(x, absmax)
     rows, cols = x.shape
     kprime = lifted_width(cols, z, l)
     kp = round_up(kprime, 256) if kp is None else kp
@@ -400,8 +409,14 @@ def fused_quant_slide(x: torch.Tensor, z: int, l: int, kind: int = QUANT_INT8, k
         _require_buffer(scales, "scales", (torch.float32,), (rows,), x.device)
     bad = C.c_int64(-1)
     ws = _status_ws(x.device) if check else None
-    st = lib().slsp_fused_quant_slide(_in_dtype(x), _ptr(x), rows, cols, z, l, kind, kp, _ptr(payload),
-                                      _ptr(scales), _ptr(ws), C.byref(bad), _stream(x.device))
+    if absmax is not None:
+        _require_scales(absmax, "absmax", rows, x.device)
+        st = lib().slsp_fused_quant_slide_scaled(_in_dtype(x), _ptr(x), rows, cols, z, l, kind, kp, _ptr(absmax),
+                                                 _ptr(payload), _ptr(scales), _ptr(ws), C.byref(bad),
+                                                 _stream(x.device))
+    else:
+        st = lib().slsp_fused_quant_slide(_in_dtype(x), _ptr(x), rows, cols, z, l, kind, kp, _ptr(payload),
+                                          _ptr(scales), _ptr(ws), C.byref(bad), _stream(x.device))
     _check(st, "fused_quant_slide", f"non-finite activation value in row {bad.value}"
            if st == ERR_NON_FINITE else None)
     # QuantizedLiftedActivation's kind and pattern (quantize.hpp:101-116) travel
@@ -509,9 +524,13 @@ def _check_pairing(w: "PackedWeights", act: torch.Tensor) -> None:
 
 def sparse_gemm(w: PackedWeights, act: torch.Tensor, s_ch: torch.Tensor | None = None,
                 s_tok: torch.Tensor | None = None, out_mode: int = OUT_RAW_NM,
-                out: torch.Tensor | None = None) -> torch.Tensor:
-    """gemm.hpp:199-233 on tcgen05.mma.sp. act: m x kp bytes (or the uint32 payload)."""
-    _require_cuda(act, s_ch, s_tok)
+                out: torch.Tensor | None = None, tok_amax: torch.Tensor | None = None) -> torch.Tensor:
+    """gemm.hpp:199-233 on tcgen05.mma.sp. act: m x kp bytes (or the uint32 payload).
+
+    tok_amax (fp32, m; BF16 outputs only): also written with each token's
+    max |y| over the n outputs, the |x|max the next layer's
+    fused_quant_slide(y, ..., absmax=tok_amax) needs (SURVEY §8f #3)."""
+    _require_cuda(act, s_ch, s_tok, tok_amax)
     m = act.shape[0]
     if act.shape[1] * act.element_size() != w.kp * w.values.element_size():
         raise DimensionMismatchError("lifted activation width does not match compressed weights")
@@ -520,6 +539,14 @@ def sparse_gemm(w: PackedWeights, act: torch.Tensor, s_ch: torch.Tensor | None =
     _require_scales(s_tok, "s_tok", m, act.device)
     o = _gemm_out(out_mode, w.n, m, w.values.dtype == torch.int8, act.device, out)
     ldo = o.shape[1]
+    if tok_amax is not None:
+        if out_mode == OUT_RAW_NM:
+            raise ValueError("tok_amax needs a BF16 output mode")
+        _require_scales(tok_amax, "tok_amax", m, act.device)
+        _check(lib().slsp_sparse_gemm_amax(w.dtype, _ptr(_raw(w.values)), _ptr(w.tiled()), w.n, w.kp, _ptr(act), m,
+                                           _ptr(s_ch), _ptr(s_tok), out_mode, _ptr(o), ldo, _ptr(tok_amax),
+                                           _stream(act.device)), "sparse_gemm")
+        return o
     wsb0 = int(lib().slsp_gemm_workspace_bytes(w.n, m))
     ws, wsb = _workspace(lambda q: lib().slsp_sparse_gemm_config(w.dtype, w.n, w.kp, m, out_mode, wsb0, q),
                          act.device)

@@ -39,7 +39,7 @@ constexpr int kNumThreads = 192;
 // emulation: the L2 traffic of a kernel that builds those stages in smem).
 // bit6 (LIFT) skips the C-block build, bit7 (LIFT) skips its proxy fence.
 enum : uint32_t { kDbgNoStore = 1u, kDbgNoLoad = 2u, kDbgSameTile = 4u, kDbgNoMeta = 8u, kDbgNoMma = 16u,
-                  kDbgSkipB3 = 32u, kDbgNoBuild = 64u, kDbgNoFence = 128u };
+                  kDbgSkipB3 = 32u, kDbgNoBuild = 64u, kDbgNoFence = 128u, kDbgNoAmaxAtomic = 256u };
 // L2 cache-policy hints (env SLSP_GEMM_HINTS overrides kDefaultHints).
 enum : uint32_t { kHintBLast = 1u, kHintAFirst = 2u, kHintOutFirst = 4u };
 constexpr uint32_t kDefaultHints = kHintBLast | kHintOutFirst;
@@ -143,7 +143,16 @@ struct Cfg {
   // REG: s_tok slice + one 32x32 BF16 staging box per warp
   static constexpr int EPI_WARP = REG_EPI ? H0 * 4 + 32 * 64 : EPI_BUFS * EPI_BUF;
   // smem ring depth: STAGES_ if given, else as many stages as fit (<= 8)
-  static constexpr int FIXED_SMEM = EPI_WARPS * EPI_WARP + 4 * 8 + 16 + 1024;
+  static constexpr int FIXED_SMEM0 = EPI_WARPS * EPI_WARP + 4 * 8 + 16 + 1024;
+  static constexpr int FIT0 = (227 * 1024 - FIXED_SMEM0) / (STAGE_TX + 16);
+  // §8f #3 token |y|max fold (BF16 outputs): a per-CTA [2][BN] merge buffer
+  // where it costs no ring stage; otherwise the fold goes to global atomics
+  // per warp
+  static constexpr int AMAX_CAND = SPARSE && OUT != SLSP_OUT_RAW_NM ? 2 * BN * 4 : 0;
+  static constexpr bool AMAX_SM =
+      AMAX_CAND > 0 && (227 * 1024 - FIXED_SMEM0 - AMAX_CAND) / (STAGE_TX + 16) >= (FIT0 < 8 ? FIT0 : 8);
+  static constexpr int AMAX_BYTES = AMAX_SM ? AMAX_CAND : 0;
+  static constexpr int FIXED_SMEM = FIXED_SMEM0 + AMAX_BYTES;
   static constexpr int FIT = (227 * 1024 - FIXED_SMEM) / (STAGE_TX + 16);
   static constexpr int STAGES = STAGES_ ? STAGES_ : (FIT < 8 ? FIT : 8);
   static_assert(STAGES >= 2, "pipeline depth");
@@ -153,7 +162,8 @@ struct Cfg {
   static constexpr int OFF_B = OFF_A + STAGES * A_STAGE;
   static constexpr int OFF_E = OFF_B + STAGES * B_STAGE;
   static constexpr int OFF_EPI = OFF_E + STAGES * E_STAGE;
-  static constexpr int OFF_BAR = OFF_EPI + EPI_WARPS * EPI_WARP;
+  static constexpr int OFF_AMAX = OFF_EPI + EPI_WARPS * EPI_WARP;
+  static constexpr int OFF_BAR = OFF_AMAX + AMAX_BYTES;
   // Two-subtile stages signal subtile 1's operands (A1, E1) on a second
   // barrier, so subtile 0's MMAs start once B, A0 and E0 have landed.
   static constexpr bool SPLIT = MSUB == 2 && SPARSE && !LIFT;
@@ -200,7 +210,99 @@ struct Params {
   int pace_ns;   // REG epilogue: sleep between output boxes (env SLSP_GEMM_PACE, perf probing)
   void* ws;
   int64_t ws_cap;  // workspace bytes (bounds ksplit)
+  // SURVEY §8f #3 (lift fused upstream): BF16 outputs also fold max |y| of
+  // every token (over this launch's output features) into amax[t] (float
+  // bits; atomicMax on the bit pattern is exact for non-negative values, and
+  // a NaN |y| (0x7FC0.. > Inf) wins, so the consumer sees the row as
+  // non-finite). The next layer's lift then needs no |x|max pass of its own.
+  uint32_t* amax;
 };
+
+// Fold |bf16| of 2*NW token columns (packed in w, token i = half i&1 of
+// w[i>>1]) over the warp's 32 rows (lanes): sm != 0 -> max into the CTA's
+// shared [BN] merge buffer at column c0 + i (flushed to p.amax once per tile
+// by fold_flush), else straight into p.amax[t0 + i]. Lanes whose rows are
+// past n hold zeros (their scale is 0), so they are neutral.
+template <int NW>
+SLSP_DEVINL void fold_token_amax(const Params& p, const uint32_t (&w)[NW], int64_t t0, uint32_t sm = 0,
+                                 int c0 = 0) {
+  constexpr int NC = 2 * NW;
+  const uint32_t lane = lane_id();
+  if constexpr (NW == 8) {
+    // 16 tokens: transposing butterfly on packed |bf16| pairs (9 shuffles +
+    // 9 per-halfword max) instead of 16 warp reductions; afterwards lane L
+    // holds the column max of token pair (L >> 2) & 7, four lanes each
+    uint32_t v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = w[i] & 0x7FFF7FFFu;
+    const bool b4 = lane & 16u, b3 = lane & 8u, b2 = lane & 4u;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t keep = b4 ? v[i + 4] : v[i], send = b4 ? v[i] : v[i + 4];
+      v[i] = __vmaxu2(keep, __shfl_xor_sync(0xffffffffu, send, 16));
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const uint32_t keep = b3 ? v[i + 2] : v[i], send = b3 ? v[i] : v[i + 2];
+      v[i] = __vmaxu2(keep, __shfl_xor_sync(0xffffffffu, send, 8));
+    }
+    uint32_t x;
+    {
+      const uint32_t keep = b2 ? v[1] : v[0], send = b2 ? v[0] : v[1];
+      x = __vmaxu2(keep, __shfl_xor_sync(0xffffffffu, send, 4));
+    }
+    x = __vmaxu2(x, __shfl_xor_sync(0xffffffffu, x, 2));
+    x = __vmaxu2(x, __shfl_xor_sync(0xffffffffu, x, 1));
+    if ((lane & 3u) < 2u && !(p.debug & kDbgNoAmaxAtomic)) {
+      const int col = 2 * static_cast<int>((lane >> 2) & 7u) + static_cast<int>(lane & 1u);
+      const uint32_t val = (lane & 1u) ? (x & 0xFFFF0000u) : (x << 16);
+      if (t0 + col < p.m) {
+        if (sm) asm volatile("red.shared.max.u32 [%0], %1;" ::"r"(sm + 4u * (c0 + col)), "r"(val) : "memory");
+        else atomicMax(p.amax + t0 + col, val);
+      }
+    }
+    return;
+  }
+  uint32_t mine[(NC + 31) / 32];
+#pragma unroll
+  for (int j = 0; j < (NC + 31) / 32; ++j) mine[j] = 0;
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    const uint32_t h = (w[i >> 1] >> (16 * (i & 1))) & 0x7FFFu;
+    const uint32_t mx = __reduce_max_sync(0xffffffffu, h);
+    if (lane == static_cast<uint32_t>(i & 31)) mine[i >> 5] = mx;
+  }
+#pragma unroll
+  for (int j = 0; j < (NC + 31) / 32; ++j) {
+    const int64_t t = t0 + 32 * j + lane;
+    if (32 * j + static_cast<int>(lane) < NC && t < p.m && !(p.debug & kDbgNoAmaxAtomic)) {
+      if (sm) asm volatile("red.shared.max.u32 [%0], %1;" ::"r"(sm + 4u * (c0 + 32 * j + lane)), "r"(mine[j] << 16)
+                           : "memory");
+      else atomicMax(p.amax + t, mine[j] << 16);
+    }
+  }
+}
+
+// Epilogue warps only (named barrier 1).
+template <int NT>
+SLSP_DEVINL void epi_bar() {
+  asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+}
+
+// After every epilogue warp folded tile `it` into merge buffer it&1: one
+// warp moves the BN column maxima to p.amax (one atomic per token per CTA)
+// and clears the buffer for tile it+2 (tile it+1 uses the other one).
+template <int BN, int NT>
+SLSP_DEVINL void fold_flush(const Params& p, uint32_t* buf, int64_t tcol0, bool first_warp) {
+  epi_bar<NT>();
+  if (first_warp) {
+    for (int c = static_cast<int>(lane_id()); c < BN; c += 32) {
+      const uint32_t v = buf[c];
+      if (v && tcol0 + c < p.m && !(p.debug & kDbgNoAmaxAtomic)) atomicMax(p.amax + tcol0 + c, v);
+      buf[c] = 0;
+    }
+  }
+}
 
 // Perf probing: slot `slot` of tile iteration `it` on CTA 0 (16 slots per tile;
 // 8/9 hold the MMA's full-wait and the producer's empty-wait cycles of the tile).
@@ -321,7 +423,8 @@ SLSP_DEVINL void dequant16(const Params& p, const uint32_t (&r)[16], float sc, i
 // with one bulk tensor store.
 template <typename C>
 SLSP_DEVINL void epilogue_chunk(const Params& p, const CUtensorMap* tmOut, uint8_t* stage,
-                                uint32_t (&r)[C::EPI_COLS], int64_t row0, int64_t t0, float sc) {
+                                uint32_t (&r)[C::EPI_COLS], int64_t row0, int64_t t0, float sc, uint32_t amax_sm,
+                                int c0) {
   constexpr int NC = C::EPI_COLS;
   constexpr int NW = C::OUT == SLSP_OUT_RAW_NM ? NC : NC / 2;  // 32-bit output words per lane
   const uint32_t lane = lane_id();
@@ -349,6 +452,8 @@ SLSP_DEVINL void epilogue_chunk(const Params& p, const CUtensorMap* tmOut, uint8
       w[i] = pack_bf16(lo, hi);
     }
   }
+  if constexpr (C::OUT != SLSP_OUT_RAW_NM)
+    if (p.amax) fold_token_amax<NW>(p, w, t0, amax_sm, c0);
   if (p.debug & kDbgNoStore) return;
 
   if (p.tma_store) {
@@ -473,6 +578,8 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     if (p.tma_store) tma_prefetch(&tmOut);
   }
   if (warp == 1) tmem_alloc<2>(tmem_slot, C::TMEM_COLS);
+  if constexpr (C::AMAX_SM)
+    for (int i = threadIdx.x; i < 2 * C::BN; i += C::THREADS) reinterpret_cast<uint32_t*>(smem + C::OFF_AMAX)[i] = 0;
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
@@ -898,9 +1005,9 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         if (warp == 2 && lane == 0) SLSP_TRACE(it, 4 + 2 * h);
       };
       auto store = [&](int h, const uint32_t (&pk)[NCH][8]) {
-        if (p.debug & kDbgNoStore) return;
         const int64_t rq = rowq + h * 256;
         if (rq >= p.n) return;  // warp-uniform
+        if (p.debug & kDbgNoStore) return;
         if (p.tma_store) {
           const uint32_t sb = smem_u32(stage);
 #pragma unroll
@@ -949,6 +1056,21 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         tc_fence_after();
       }
       drain(1, sc1, pk1);
+      if (p.amax) {  // §8f #3: both subtiles' rows, then across lanes and warps
+        const uint32_t sm = C::AMAX_SM ? smem_u32(smem + C::OFF_AMAX) + (it & 1) * C::BN * 4 : 0u;
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+          if (c < nch) {
+            uint32_t mx[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) mx[i] = __vmaxu2(pk0[c][i] & 0x7FFF7FFFu, pk1[c][i] & 0x7FFF7FFFu);
+            fold_token_amax<8>(p, mx, tcol0 + 16 * c, sm, static_cast<int>(half) * C::H0 + 16 * c);
+          }
+        }
+        if constexpr (C::AMAX_SM)
+          fold_flush<C::BN, C::EPI_WARPS * 32>(p, reinterpret_cast<uint32_t*>(smem + C::OFF_AMAX) + (it & 1) * C::BN,
+                                               static_cast<int64_t>(nt) * C::BN, warp == 2);
+      }
       store(0, pk0);
       if (warp == 2 && lane == 0) SLSP_TRACE(it, 5);
       store(1, pk1);
@@ -1013,13 +1135,19 @@ __global__ void __launch_bounds__(C::THREADS, 1)
             if (lane == 0) bulk_wait_read<C::EPI_BUFS - 1>();  // staging buffer free again
             __syncwarp();
           }
-          epilogue_chunk<C>(p, &tmOut, stage_base + buf * C::EPI_BUF, r, row0, t0, sc);
+          epilogue_chunk<C>(p, &tmOut, stage_base + buf * C::EPI_BUF, r, row0, t0, sc,
+                            C::AMAX_SM ? smem_u32(smem + C::OFF_AMAX) + (it & 1) * C::BN * 4 : 0u,
+                            c * C::EPI_COLS);
           if (C::EPI_BUFS == 2) buf ^= 1;
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[C::MSUB == 2 ? h : acc]), lead));
       }
+      if constexpr (C::AMAX_SM)
+        if (p.amax)
+          fold_flush<C::BN, C::EPI_WARPS * 32>(p, reinterpret_cast<uint32_t*>(smem + C::OFF_AMAX) + (it & 1) * C::BN,
+                                               static_cast<int64_t>(nt) * C::BN, warp == 2);
     }
     if (lane == 0) bulk_wait<0>();
   }
@@ -1385,11 +1513,13 @@ int check_out(int out_mode, const float* s_ch, const float* s_tok, void* out, in
 template <bool LIFT>
 int sparse_entry(int dtype, const void* values, const uint8_t* meta, int64_t n, int64_t kp, const void* act,
                  int64_t act_row, int64_t m, const float* s_ch, const float* s_tok, int out_mode, void* out,
-                 int64_t ldo, slsp_stream_t stream, void* ws, int64_t ws_bytes, slsp_gemm_config* q = nullptr) {
+                 int64_t ldo, slsp_stream_t stream, void* ws, int64_t ws_bytes, slsp_gemm_config* q = nullptr,
+                 float* tok_amax = nullptr) {
   using namespace slsp_host;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (n < 0 || m < 0 || kp <= 0) return SLSP_ERR_INVALID;
   if (kp % 256 != 0) return SLSP_ERR_DIMENSION;
+  if (tok_amax && out_mode == SLSP_OUT_RAW_NM) return SLSP_ERR_INVALID;  // |y| max of the BF16 outputs
   if (kp > (int64_t{1} << 23)) return SLSP_ERR_INVALID;  // gemm.hpp:56 int8 accumulator bound
   if (n > (int64_t{1} << 31) - 256 || m > (int64_t{1} << 31) - 256) return SLSP_ERR_UNSUPPORTED;
   int st = SLSP_OK;
@@ -1420,9 +1550,13 @@ int sparse_entry(int dtype, const void* values, const uint8_t* meta, int64_t n, 
                                (msub == 1 && m <= kBn256MaxM && env_knob("SLSP_GEMM_KHALF1", kSparseKHalf1)))
                           ? 1u
                           : 0u;
-  if (ws && ws_bytes >= 2 * n * m * 4) {  // split-K partial-sum slices
+  if (ws && ws_bytes >= 2 * n * m * 4 && !tok_amax) {  // split-K partial-sum slices (not with the amax fold)
     p.ws = ws;
     p.ws_cap = ws_bytes;
+  }
+  if (tok_amax && !q) {  // the fold max-accumulates into zeros
+    SLSP_CUDA_TRY(cudaMemsetAsync(tok_amax, 0, static_cast<size_t>(m) * sizeof(float), s));
+    p.amax = reinterpret_cast<uint32_t*>(tok_amax);
   }
   if (!q) {
     if ((st = make_map_2d(&tb, act, act_row * esz, m, bn / 2))) return st;
@@ -1543,6 +1677,14 @@ int slsp_sparse_gemm_ws(int dtype, const void* values, const uint8_t* meta, int6
                         void* workspace, int64_t ws_bytes, slsp_stream_t stream) {
   return sparse_entry<false>(dtype, values, meta, n, kp, act, kp, m, s_ch, s_tok, out_mode, out, ldo, stream, workspace,
                              ws_bytes);
+}
+
+int slsp_sparse_gemm_amax(int dtype, const void* values, const uint8_t* meta, int64_t n, int64_t kp, const void* act,
+                          int64_t m, const float* s_ch, const float* s_tok, int out_mode, void* out, int64_t ldo,
+                          float* tok_amax, slsp_stream_t stream) {
+  if (!tok_amax) return SLSP_ERR_INVALID;
+  return sparse_entry<false>(dtype, values, meta, n, kp, act, kp, m, s_ch, s_tok, out_mode, out, ldo, stream, nullptr,
+                             0, nullptr, tok_amax);
 }
 
 int64_t slsp_gemm_workspace_bytes(int64_t n, int64_t m) {

@@ -38,6 +38,9 @@ struct ActArgs {
   uint8_t* out;
   float* scales;
   unsigned long long* status;
+  // §8f #3: each row's |x|max computed upstream (slsp_sparse_gemm_amax);
+  // when set, the kernels skip their own |x|max pass / block reduction
+  const float* amax_in;
 };
 
 // Launch-path selection (env SLSP_LIFT_ROW, perf probing): 0 = warp path,
@@ -112,6 +115,10 @@ __global__ void __launch_bounds__(kThreads) act_kernel(ActArgs a) {
     for (int i = 0; i < kThreads / 32; ++i) {
       amax = fmaxf(amax, s_red[i]);
       bad |= s_bad[i];
+    }
+    if (a.amax_in) {
+      amax = a.amax_in[row];
+      bad = !isfinite(amax);
     }
     if (bad && threadIdx.x == 0 && a.status) atomicMin(a.status, static_cast<unsigned long long>(row) << 32);
 
@@ -335,7 +342,10 @@ __global__ void __launch_bounds__(256) act_warp_kernel(ActArgs a) {
     if constexpr (KIND != K_NONE) {
       float amax = 0.f;
       int bad = 0;
-      if constexpr (IN == IN_BF16) {
+      if (a.amax_in) {
+        amax = a.amax_in[row];
+        bad = !isfinite(amax);
+      } else if constexpr (IN == IN_BF16) {
         // packed bf16x2 |x| max; NaN propagates and Inf wins, so the row is
         // non-finite iff the final max is
         __nv_bfloat162 m2 = __float2bfloat162_rn(0.f);
@@ -365,10 +375,12 @@ __global__ void __launch_bounds__(256) act_warp_kernel(ActArgs a) {
           }
         }
       }
+      if (!a.amax_in) {
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-        bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+        for (int o = 16; o > 0; o >>= 1) {
+          amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+          bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+        }
       }
       if (bad && lane == 0 && a.status) atomicMin(a.status, static_cast<unsigned long long>(row) << 32);
       // quantize.hpp:151-153, in double
@@ -425,6 +437,10 @@ SLSP_DEVINL void row_emit(const ActArgs& a, int64_t row, int nquads, float* s_ma
   float r32 = 0.f;
   if constexpr (KIND != K_NONE) {
     float amax;
+    if (a.amax_in) {
+      // |x|max from upstream: no block reduction, every warp runs on
+      amax = a.amax_in[row];
+    } else {
     if constexpr (IN == IN_BF16) {
       // packed bf16x2 |x| max; NaN propagates and Inf wins, so the row is
       // non-finite iff the final max is (zero-filled tail slots are neutral)
@@ -465,6 +481,7 @@ SLSP_DEVINL void row_emit(const ActArgs& a, int64_t row, int nquads, float* s_ma
       amax = (isnan(t) || t > amax) ? t : amax;
     }
     __syncthreads();  // s_max is reused by the next row
+    }
     if (!isfinite(amax) && tid == 0 && a.status) atomicMin(a.status, static_cast<unsigned long long>(row) << 32);
     // quantize.hpp:151-153, in double
     const double qmax = KIND == K_INT8 ? 127.0 : 448.0;
@@ -686,6 +703,40 @@ int slsp_fused_quant_slide(int in_dtype, const void* x, int64_t rows, int64_t co
   a.out = reinterpret_cast<uint8_t*>(payload);
   a.scales = scales;
   a.status = ss.ptr;
+  if ((st = dispatch_quant<true>(in_dtype, kind, a, s))) return st;
+  return status_collect(status_ws, s, SLSP_ERR_NON_FINITE, bad_row, nullptr);
+}
+
+int slsp_fused_quant_slide_scaled(int in_dtype, const void* x, int64_t rows, int64_t cols, int z, int l, int kind,
+                                  int64_t kp, const float* tok_amax, uint32_t* payload, float* scales, void* status_ws,
+                                  int64_t* bad_row, slsp_stream_t stream) {
+  using namespace slsp_host;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int wc = 0;
+  int st = plan(z, l, &wc);
+  if (st) return st;
+  if ((in_dtype != SLSP_DT_F32 && in_dtype != SLSP_DT_BF16) || (kind != 0 && kind != 1)) return SLSP_ERR_INVALID;
+  if (rows < 0 || cols < 0 || (rows > 0 && !tok_amax)) return SLSP_ERR_INVALID;
+  const int64_t groups = (cols + l - 1) / l;
+  const int64_t words = groups * wc;
+  if (kp < words * 4 || kp % 16 != 0) return SLSP_ERR_DIMENSION;
+  if ((st = require_sm100())) return st;
+  StatusScope ss;
+  if ((st = ss.init(status_ws, s))) return st;
+  ActArgs a{};
+  a.x = static_cast<const uint8_t*>(x);
+  a.rows = rows;
+  a.cols = cols;
+  a.l = l;
+  a.wc = wc;
+  a.kind = kind;
+  a.in_cols_pad = groups * l;
+  a.words_real = words;
+  a.out_bytes = kp;
+  a.out = reinterpret_cast<uint8_t*>(payload);
+  a.scales = scales;
+  a.status = ss.ptr;
+  a.amax_in = tok_amax;
   if ((st = dispatch_quant<true>(in_dtype, kind, a, s))) return st;
   return status_collect(status_ws, s, SLSP_ERR_NON_FINITE, bad_row, nullptr);
 }
