@@ -175,6 +175,19 @@ def run_b200(args, world, rank, local):
     # replicated on every rank (same seed)
     xgen = torch.Generator(device=device).manual_seed(99)
     xs = [(torch.rand((m, L.k), device=device, generator=xgen) * 2 - 1).to(torch.bfloat16) for L in layers]
+    # N>1: each layer's input arrives K-sharded (the previous layer's output
+    # features are spread over the ranks); the sharded lift lifts
+    # this rank's column slice with the all-reduced |x|max straight into every
+    # rank's payload over NVLink (CUDA IPC peer writes), so each rank lifts
+    # 1/world of X and no all-gather of X or of the payload follows
+    sliced = []
+    if world > 1:
+        from paper_2603_05232_b200.sharding import ShardedLift
+
+        for i, L in enumerate(layers):
+            L.sl = ShardedLift(m, L.k, z, l, L.kp, world, rank, device)
+            L.payload, L.s_tok = L.sl.payload, L.sl.scales
+            sliced.append(xs[i][:, L.sl.k0:L.sl.k1].contiguous())
     outs = [torch.empty((L.n, m) if out_mode == slsp.OUT_BF16_NM else (m, L.n), dtype=torch.bfloat16,
                         device=device) for L in layers]
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=device)
@@ -182,6 +195,8 @@ def run_b200(args, world, rank, local):
     # Each kernel call of the step is captured into a CUDA graph, so the timed
     # region measures device time, not Python launch latency.
     def op_lift(L, i):
+        if world > 1:
+            return lambda: L.sl(sliced[i])
         return lambda: slsp.fused_quant_slide(xs[i], z, l, kp=L.kp, check=False, payload=L.payload,
                                               scales=L.s_tok)
 
@@ -202,12 +217,27 @@ def run_b200(args, world, rank, local):
         f()
     torch.cuda.synchronize()
 
-    def capture(fns):
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            for f in fns:
+    class Eager:  # stand-in when a multi-rank step cannot be graph-captured (NCCL / driver without support)
+        def __init__(self, fns):
+            self.fns = fns
+
+        def replay(self):
+            for f in self.fns:
                 f()
-        return g
+
+    def capture(fns):
+        try:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                for f in fns:
+                    f()
+            return g
+        except Exception as e:  # noqa: BLE001
+            if world == 1:
+                raise
+            print(f"[bench rank {rank}] graph capture failed ({e}); timing eager launches", file=sys.stderr)
+            torch.cuda.synchronize()
+            return Eager(fns)
 
     sparse_graph = capture(sparse_ops)
     dense_graph = capture(dense_ops) if dense_ops else None
@@ -358,7 +388,10 @@ def run_b200(args, world, rank, local):
                 "X = U(-1,1) bf16, seeded",
         "config": {"workload": f"{args.workload} all linear shapes, {args.pattern} INT8 W8A8, M={m} prefill",
                    "m": m, "pattern": args.pattern, "layers": [f"{n}x{k}" for _, n, k in WORKLOADS[args.workload]],
-                   "step": "per layer: fused_quant_slide(bf16 X) + sparse GEMM, bf16 dequant epilogue",
+                   "step": "per layer: fused_quant_slide(bf16 X) + sparse GEMM, bf16 dequant epilogue" if world == 1
+                   else "per layer: sharded lift (row_absmax of this rank's K-slice, NCCL all_reduce MAX, "
+                        "lift into every rank's payload over NVLink IPC, NCCL barrier) + sparse GEMM on the "
+                        "rank's N-shard; dense step: replicated quantize_rows + dense GEMM",
                    "out_layout": args.out_mode, "parallelism": f"N-shard x{world}" if world > 1 else "single",
                    "l2": "flushed between timed steps (512 MiB write, outside events)"},
         "speedup_vs_dense": round(de_ms_max / sp_ms_max, 4) if de_ms_max else None,

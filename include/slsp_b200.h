@@ -187,6 +187,34 @@ SLSP_API int slsp_fused_quant_slide_scaled(int in_dtype, const void* x, int64_t 
                                            int kind, int64_t kp, const float* tok_amax, uint32_t* payload,
                                            float* scales, void* status_ws, int64_t* bad_row, slsp_stream_t stream);
 
+/* Sharded lift. The input X of an N-sharded layer
+ * arrives K-sharded (rank r holds columns [k0, k0+cols) — the previous
+ * layer's output features it computed). Each rank:
+ *   slsp_row_absmax          its slice's per-row |x|max (or the tok_amax of
+ *                            slsp_sparse_gemm_amax when it produced the slice),
+ *   all-reduce(MAX) over ranks (M floats; exact),
+ *   slsp_fused_quant_slide_scaled_multi
+ *                            quantizes + lifts its slice with the global
+ *                            |x|max and writes the lifted bytes — byte column
+ *                            dst_col = k0*K'/K of the full payload row (row
+ *                            stride dst_ld = kp) — into EVERY rank's payload
+ *                            (dsts: this rank's buffer first, then the peers',
+ *                            opened with slsp_ipc_open_handle), so no
+ *                            all-gather follows; a stream-ordered barrier
+ *                            before the GEMM reads the assembled payload.
+ * The assembled payload and scales equal slsp_fused_quant_slide on the full
+ * X byte for byte. cols % (4*l) == 0; padding past K' (kp > K') is the
+ * caller's (zero it once). */
+SLSP_API int slsp_row_absmax(int in_dtype, const void* x, int64_t rows, int64_t cols, float* amax,
+                             slsp_stream_t stream);
+SLSP_API int slsp_fused_quant_slide_scaled_multi(int in_dtype, const void* x, int64_t rows, int64_t cols, int z, int l,
+                                                 int kind, const float* tok_amax, void* const* dsts, int ndst,
+                                                 int64_t dst_ld, int64_t dst_col, float* scales, void* status_ws,
+                                                 int64_t* bad_row, slsp_stream_t stream);
+SLSP_API int slsp_ipc_get_handle(const void* ptr, void* handle_out, int64_t* offset_out);
+SLSP_API int slsp_ipc_open_handle(const void* handle, void** ptr_out);
+SLSP_API int slsp_ipc_close(void* ptr);
+
 /* SLSP kind-2 container payload -> MMA-ready weights (
  * container.hpp:379-390 to_container / :424-435 compressed_from). values:
  * the container's values section on the device (rows x windows x 2 elements);

@@ -8,9 +8,9 @@ from ._native import (  # noqa: F401
     DT_BF16, DT_E4M3, DT_F32, DT_F64, DT_I8, OUT_BF16_MN, OUT_BF16_NM, OUT_RAW_NM, QUANT_FP8E4M3, QUANT_INT8,
     CudaError, DimensionMismatchError, GemmOrderWeights, MalformedMetadataError, NonFiniteInputError, NotCompliantError,
     PackedWeights, PlanError, SlspError, UnsupportedError, compress, dense_gemm, dense_gemm_config, device_supported,
-    fused_quant_slide, gemm_order, knobs, lib, lift_rows, lifted_width, magnitude_prune, pack_compress, pack_matrix,
-    plan_decomposition, quantize_rows, reload_knobs, round_up, sparse_gemm, sparse_gemm_config, sparse_gemm_x,
-    tile_meta,
+    fused_quant_slide, fused_quant_slide_multi, gemm_order, ipc_close, ipc_handle, ipc_open, knobs, lib, lift_rows,
+    lifted_width, magnitude_prune, pack_compress, pack_matrix, plan_decomposition, quantize_rows, reload_knobs,
+    round_up, row_absmax, sparse_gemm, sparse_gemm_config, sparse_gemm_x, tile_meta,
 )
 
 from . import container  # noqa: F401,E402

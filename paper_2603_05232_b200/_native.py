@@ -126,6 +126,12 @@ def lib() -> C.CDLL:
                 "slsp_sparse_gemm_amax": (i32, [i32, vp, vp, i64, i64, vp, i64, vp, vp, i32, vp, i64, vp, vp]),
                 "slsp_fused_quant_slide_scaled": (i32, [i32, vp, i64, i64, i32, i32, i32, i64, vp, vp, vp, vp, vp,
                                                         vp]),
+                "slsp_fused_quant_slide_scaled_multi": (i32, [i32, vp, i64, i64, i32, i32, i32, vp, vp, i32, i64,
+                                                              i64, vp, vp, vp, vp]),
+                "slsp_row_absmax": (i32, [i32, vp, i64, i64, vp, vp]),
+                "slsp_ipc_get_handle": (i32, [vp, vp, vp]),
+                "slsp_ipc_open_handle": (i32, [vp, vp]),
+                "slsp_ipc_close": (i32, [vp]),
                 "slsp_tiled_meta_bytes": (i64, [i64, i64]),
                 "slsp_reload_knobs": (None, []),
                 "slsp_sparse_gemm_config": (i32, [i32, i64, i64, i64, i32, i64, C.POINTER(GemmConfig)]),
@@ -425,6 +431,61 @@ def fused_quant_slide(x: torch.Tensor, z: int, l: int, kind: int = QUANT_INT8, k
     payload.slsp_kind = kind
     payload.slsp_pattern = (z, l)
     return payload, scales
+
+
+def row_absmax(x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Per-row max |x| (fp32; NaN propagates): a rank's partial |x|max in the sharded lift."""
+    _require_cuda(x)
+    rows, cols = x.shape
+    if out is None:
+        out = torch.empty(rows, dtype=torch.float32, device=x.device)
+    else:
+        _require_buffer(out, "out", (torch.float32,), (rows,), x.device)
+    _check(lib().slsp_row_absmax(_in_dtype(x), _ptr(x), rows, cols, _ptr(out), _stream(x.device)), "row_absmax")
+    return out
+
+
+def fused_quant_slide_multi(x: torch.Tensor, z: int, l: int, absmax: torch.Tensor, dsts: list, dst_ld: int,
+                            dst_col: int, kind: int = QUANT_INT8, scales: torch.Tensor | None = None,
+                            check: bool = True) -> torch.Tensor:
+    """Lift a K-slice of X (rows x cols) with the global per-row |x|max into the
+    byte column dst_col (row stride dst_ld bytes) of every payload in `dsts`
+    (device pointers or tensors; the first is this device's, the rest may be
+    peer mappings from ipc_open). Returns the scales (identical on every rank)."""
+    _require_cuda(x, absmax)
+    rows, cols = x.shape
+    _require_scales(absmax, "absmax", rows, x.device)
+    if scales is None:
+        scales = torch.empty(rows, dtype=torch.float32, device=x.device)
+    ptrs = (C.c_void_p * len(dsts))(*[d.data_ptr() if isinstance(d, torch.Tensor) else int(d) for d in dsts])
+    bad = C.c_int64(-1)
+    ws = _status_ws(x.device) if check else None
+    st = lib().slsp_fused_quant_slide_scaled_multi(_in_dtype(x), _ptr(x), rows, cols, z, l, kind, _ptr(absmax), ptrs,
+                                                   len(dsts), dst_ld, dst_col, _ptr(scales), _ptr(ws), C.byref(bad),
+                                                   _stream(x.device))
+    _check(st, "fused_quant_slide_multi", f"non-finite activation value in row {bad.value}"
+           if st == ERR_NON_FINITE else None)
+    return scales
+
+
+def ipc_handle(t: torch.Tensor) -> tuple[bytes, int]:
+    """(CUDA IPC handle of the allocation holding t, byte offset of t in it)."""
+    buf = C.create_string_buffer(64)
+    off = C.c_int64(0)
+    _check(lib().slsp_ipc_get_handle(C.c_void_p(t.data_ptr()), buf, C.byref(off)), "ipc_handle")
+    return buf.raw, int(off.value)
+
+
+def ipc_open(handle: tuple[bytes, int]) -> tuple[int, int]:
+    """Maps a peer's (handle, offset) into this process -> (base, tensor pointer)."""
+    raw, off = handle
+    ptr = C.c_void_p()
+    _check(lib().slsp_ipc_open_handle(C.create_string_buffer(raw, 64), C.byref(ptr)), "ipc_open")
+    return int(ptr.value), int(ptr.value) + off
+
+
+def ipc_close(base: int) -> None:
+    _check(lib().slsp_ipc_close(C.c_void_p(base)), "ipc_close")
 
 
 def quantize_rows(x: torch.Tensor, kind: int = QUANT_INT8, kpad: int | None = None,

@@ -41,7 +41,21 @@ struct ActArgs {
   // §8f #3: each row's |x|max computed upstream (slsp_sparse_gemm_amax);
   // when set, the kernels skip their own |x|max pass / block reduction
   const float* amax_in;
+  // Row stride of the output(s) in bytes (== out_bytes except for the
+  // K-sharded multi-destination lift, where a rank writes its column slice
+  // of every rank's full payload: out and dst[0..ndst) all at the slice's
+  // byte column, ld = the full payload row, SURVEY §8e / DESIGN §7)
+  int64_t out_ld;
+  int ndst;
+  uint8_t* dst[7];
 };
+
+// 16-byte store of output vector `i` of row `row` to the output and every
+// extra destination (peer payloads over NVLink in the sharded lift).
+SLSP_DEVINL void store_out_vec(const ActArgs& a, int64_t row, int i, uint4 v) {
+  reinterpret_cast<uint4*>(a.out + row * a.out_ld)[i] = v;
+  for (int d = 0; d < a.ndst; ++d) reinterpret_cast<uint4*>(a.dst[d] + row * a.out_ld)[i] = v;
+}
 
 // Launch-path selection (env SLSP_LIFT_ROW, perf probing): 0 = warp path,
 // else (default) the row-resident path where it applies. (Measured and
@@ -135,7 +149,7 @@ __global__ void __launch_bounds__(kThreads) act_kernel(ActArgs a) {
     __syncthreads();
 
     // ---- pass 3: emit the row, 16 bytes per thread per step ----
-    uint8_t* dst = a.out + row * a.out_bytes;
+    uint8_t* dst = a.out + row * a.out_ld;
     const int64_t nchunks = a.out_bytes >> 4;
     for (int64_t c = threadIdx.x; c < nchunks; c += kThreads) {
       uint32_t o[4];
@@ -336,7 +350,6 @@ __global__ void __launch_bounds__(256) act_warp_kernel(ActArgs a) {
   const int out_vecs = static_cast<int>(a.out_bytes >> 4);
   for (int64_t row = warp0; row < a.rows; row += nwarps) {
     const uint4* src = reinterpret_cast<const uint4*>(a.x + row * a.cols * G::ESZ);
-    uint4* dst = reinterpret_cast<uint4*>(a.out + row * a.out_bytes);
     double r = 0.0;
     float r32 = 0.f;
     if constexpr (KIND != K_NONE) {
@@ -399,9 +412,10 @@ __global__ void __launch_bounds__(256) act_warp_kernel(ActArgs a) {
       emit_quad<IN, KIND, L>(v, r32, r, o);
 #pragma unroll
       for (int i = 0; i < G::OUT_VEC; ++i)
-        dst[q * G::OUT_VEC + i] = make_uint4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
+        store_out_vec(a, row, q * G::OUT_VEC + i, make_uint4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]));
     }
-    for (int i = nquads * G::OUT_VEC + lane; i < out_vecs; i += 32) dst[i] = make_uint4(0, 0, 0, 0);  // kp padding
+    for (int i = nquads * G::OUT_VEC + lane; i < out_vecs; i += 32)
+      store_out_vec(a, row, i, make_uint4(0, 0, 0, 0));  // kp padding
   }
 }
 
@@ -432,7 +446,6 @@ SLSP_DEVINL void row_emit(const ActArgs& a, int64_t row, int nquads, float* s_ma
   using G = WarpGeom<IN, KIND, L>;
   const int tid = threadIdx.x;
   const int nthr = blockDim.x;
-  uint4* dst = reinterpret_cast<uint4*>(a.out + row * a.out_bytes);
   double r = 0.0;
   float r32 = 0.f;
   if constexpr (KIND != K_NONE) {
@@ -498,10 +511,11 @@ SLSP_DEVINL void row_emit(const ActArgs& a, int64_t row, int nquads, float* s_ma
     emit_quad<IN, KIND, L>(v[j], r32, r, o);
 #pragma unroll
     for (int i = 0; i < G::OUT_VEC; ++i)
-      dst[q * G::OUT_VEC + i] = make_uint4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
+      store_out_vec(a, row, q * G::OUT_VEC + i, make_uint4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]));
   }
   const int out_vecs = static_cast<int>(a.out_bytes >> 4);
-  for (int i = nquads * G::OUT_VEC + tid; i < out_vecs; i += nthr) dst[i] = make_uint4(0, 0, 0, 0);  // kp padding
+  for (int i = nquads * G::OUT_VEC + tid; i < out_vecs; i += nthr)
+    store_out_vec(a, row, i, make_uint4(0, 0, 0, 0));  // kp padding
 }
 
 // MAXT/MINB: launch bounds; the <=128-thread instantiation asks for 16
@@ -659,6 +673,55 @@ int dispatch_quant(int in_dtype, int kind, ActArgs& a, cudaStream_t s) {
                                  : launch_act<IN_BF16, K_FP8, LIFT>(a, esz, s);
 }
 
+// Per-row |x|max (NaN propagates): the partial |x|max of a rank's K-slice in
+// the sharded lift (all-reduced with MAX across ranks, then fed to
+// slsp_fused_quant_slide_scaled_multi). One warp per row, 16-byte loads
+// where the row is aligned.
+template <int IN>
+__global__ void __launch_bounds__(256) row_absmax_kernel(const uint8_t* x, int64_t rows, int64_t cols, float* out) {
+  constexpr int ESZ = IN == IN_F32 ? 4 : 2;
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t row = w0; row < rows; row += nw) {
+    const uint8_t* src = x + row * cols * ESZ;
+    float m = 0.f;
+    bool nan = false;
+    int64_t done = 0;
+    if ((reinterpret_cast<uintptr_t>(src) & 15u) == 0) {
+      const int64_t nvec = cols * ESZ / 16;
+      for (int64_t i = lane; i < nvec; i += 32) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(src) + i);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if constexpr (IN == IN_F32) {
+            const float f = __uint_as_float(w[j]);
+            nan |= isnan(f);
+            m = fmaxf(m, fabsf(f));
+          } else {
+            const float f0 = __uint_as_float(w[j] << 16), f1 = __uint_as_float(w[j] & 0xFFFF0000u);
+            nan |= isnan(f0) | isnan(f1);
+            m = fmaxf(m, fmaxf(fabsf(f0), fabsf(f1)));
+          }
+        }
+      }
+      done = nvec * 16 / ESZ;
+    }
+    for (int64_t i = done + lane; i < cols; i += 32) {
+      const float f = in_value<IN>(src, i);
+      nan |= isnan(f);
+      m = fmaxf(m, fabsf(f));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      nan |= __shfl_xor_sync(0xffffffffu, nan ? 1 : 0, o) != 0;
+    }
+    if (lane == 0) out[row] = nan ? __int_as_float(0x7fc00000) : m;
+  }
+}
+
 // Status word: the caller's scratch when checking, else none (kernels skip
 // the report; the hot path stays asynchronous and graph-capturable).
 struct StatusScope {
@@ -700,6 +763,7 @@ int slsp_fused_quant_slide(int in_dtype, const void* x, int64_t rows, int64_t co
   a.in_cols_pad = groups * l;
   a.words_real = words;
   a.out_bytes = kp;
+  a.out_ld = kp;
   a.out = reinterpret_cast<uint8_t*>(payload);
   a.scales = scales;
   a.status = ss.ptr;
@@ -733,12 +797,82 @@ int slsp_fused_quant_slide_scaled(int in_dtype, const void* x, int64_t rows, int
   a.in_cols_pad = groups * l;
   a.words_real = words;
   a.out_bytes = kp;
+  a.out_ld = kp;
   a.out = reinterpret_cast<uint8_t*>(payload);
   a.scales = scales;
   a.status = ss.ptr;
   a.amax_in = tok_amax;
   if ((st = dispatch_quant<true>(in_dtype, kind, a, s))) return st;
   return status_collect(status_ws, s, SLSP_ERR_NON_FINITE, bad_row, nullptr);
+}
+
+int slsp_fused_quant_slide_scaled_multi(int in_dtype, const void* x, int64_t rows, int64_t cols, int z, int l,
+                                        int kind, const float* tok_amax, void* const* dsts, int ndst, int64_t dst_ld,
+                                        int64_t dst_col, float* scales, void* status_ws, int64_t* bad_row,
+                                        slsp_stream_t stream) {
+  using namespace slsp_host;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int wc = 0;
+  int st = plan(z, l, &wc);
+  if (st) return st;
+  if ((in_dtype != SLSP_DT_F32 && in_dtype != SLSP_DT_BF16) || (kind != 0 && kind != 1)) return SLSP_ERR_INVALID;
+  if (rows < 0 || cols < 0 || ndst < 1 || ndst > 8 || !dsts || (rows > 0 && !tok_amax)) return SLSP_ERR_INVALID;
+  const int esz = in_dtype == SLSP_DT_F32 ? 4 : 2;
+  // the slice is whole quads (4 blocks) so every rank's windows are its own
+  // and its lifted bytes are whole 16-byte vectors at a 16-byte column
+  if (cols % (4 * l) != 0 || (cols * esz) % 16 != 0) return SLSP_ERR_DIMENSION;
+  const int64_t bytes = cols / l * wc * 4;
+  if (dst_col < 0 || dst_col % 16 != 0 || dst_ld % 16 != 0 || dst_col + bytes > dst_ld) return SLSP_ERR_DIMENSION;
+  for (int d = 0; d < ndst; ++d)
+    if (!dsts[d] || (reinterpret_cast<uintptr_t>(dsts[d]) & 15u)) return SLSP_ERR_INVALID;
+  if ((st = require_sm100())) return st;
+  StatusScope ss;
+  if ((st = ss.init(status_ws, s))) return st;
+  ActArgs a{};
+  a.x = static_cast<const uint8_t*>(x);
+  a.rows = rows;
+  a.cols = cols;
+  a.l = l;
+  a.wc = wc;
+  a.kind = kind;
+  a.in_cols_pad = cols;
+  a.words_real = cols / l * wc;
+  a.out_bytes = bytes;
+  a.out_ld = dst_ld;
+  a.out = static_cast<uint8_t*>(dsts[0]) + dst_col;
+  a.ndst = ndst - 1;
+  for (int d = 1; d < ndst; ++d) a.dst[d - 1] = static_cast<uint8_t*>(dsts[d]) + dst_col;
+  a.scales = scales;
+  a.status = ss.ptr;
+  a.amax_in = tok_amax;
+  if (rows > 0) {
+    int launched = 0;
+    st = SLSP_OK;
+    if (in_dtype == SLSP_DT_BF16)
+      launched = kind == SLSP_QUANT_INT8 ? try_warp_path<IN_BF16, K_INT8>(a, s, &st)
+                                         : try_warp_path<IN_BF16, K_FP8>(a, s, &st);
+    else
+      launched = kind == SLSP_QUANT_INT8 ? try_warp_path<IN_F32, K_INT8>(a, s, &st)
+                                         : try_warp_path<IN_F32, K_FP8>(a, s, &st);
+    if (!launched) return SLSP_ERR_UNSUPPORTED;  // (no smem-path fallback for sliced writes)
+    if (st) return st;
+  }
+  return status_collect(status_ws, s, SLSP_ERR_NON_FINITE, bad_row, nullptr);
+}
+
+int slsp_row_absmax(int in_dtype, const void* x, int64_t rows, int64_t cols, float* amax, slsp_stream_t stream) {
+  using namespace slsp_host;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if ((in_dtype != SLSP_DT_F32 && in_dtype != SLSP_DT_BF16) || rows < 0 || cols < 0) return SLSP_ERR_INVALID;
+  int st;
+  if ((st = require_sm100())) return st;
+  if (rows == 0) return SLSP_OK;
+  const int64_t blocks = (rows + 7) / 8;
+  const unsigned grid = static_cast<unsigned>(blocks < 65535 * 32 ? blocks : 65535 * 32);
+  if (in_dtype == SLSP_DT_BF16) row_absmax_kernel<IN_BF16><<<grid, 256, 0, s>>>(static_cast<const uint8_t*>(x), rows, cols, amax);
+  else row_absmax_kernel<IN_F32><<<grid, 256, 0, s>>>(static_cast<const uint8_t*>(x), rows, cols, amax);
+  SLSP_LAUNCH_CHECK();
+  return SLSP_OK;
 }
 
 int slsp_quantize_rows(int in_dtype, const void* x, int64_t rows, int64_t cols, int kind, int64_t kpad, uint8_t* out,
@@ -762,6 +896,7 @@ int slsp_quantize_rows(int in_dtype, const void* x, int64_t rows, int64_t cols, 
   a.in_cols_pad = cols;
   a.words_real = 0;
   a.out_bytes = kpad;
+  a.out_ld = kpad;
   a.out = out;
   a.scales = scales;
   a.status = ss.ptr;
@@ -794,6 +929,7 @@ int slsp_lift_rows(int dtype, const void* x, int64_t rows, int64_t cols, int z, 
   a.in_cols_pad = cols;
   a.words_real = words;
   a.out_bytes = kp * esz;
+  a.out_ld = kp * esz;
   a.out = static_cast<uint8_t*>(out);
   a.status = ss.ptr;
   return dtype == SLSP_DT_BF16 ? launch_act<IN_BF16, K_NONE, true>(a, esz, s)

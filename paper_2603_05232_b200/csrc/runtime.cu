@@ -1,3 +1,5 @@
+#include <cuda.h>
+#include <mutex>
 // C-ABI plumbing: versioning, status scratch, plan geometry, device checks.
 #include <cstdio>
 #include <cstdlib>
@@ -169,6 +171,51 @@ int slsp_plan_decomposition(int z, int l, int hw_m, int hw_n, int* window_count,
     if (wc > cap) return SLSP_ERR_INVALID;
     for (int j = 0; j < wc; ++j) window_starts[j] = j * stride;
   }
+  return SLSP_OK;
+}
+
+// Multi-GPU plumbing for the sharded lift: a rank's payload
+// buffer is exported as a CUDA IPC handle (64 bytes, exchanged by the host
+// over torch.distributed) and opened by every peer on the same node, so the
+// lift kernel writes its K-slice into all ranks' payloads over NVLink.
+// The handle names the whole cudaMalloc allocation holding ptr (a caching
+// allocator hands out sub-ranges), so the byte offset of ptr inside it is
+// returned too; the peer adds it to the base slsp_ipc_open_handle maps.
+int slsp_ipc_get_handle(const void* ptr, void* handle_out, int64_t* offset_out) {
+  if (!ptr || !handle_out || !offset_out) return SLSP_ERR_INVALID;
+  using RangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static RangeFn range = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* fp = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fp, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      range = reinterpret_cast<RangeFn>(fp);
+  });
+  if (!range) return SLSP_ERR_CUDA;
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range(&base, &size, reinterpret_cast<CUdeviceptr>(ptr)) != CUDA_SUCCESS) return SLSP_ERR_CUDA;
+  cudaIpcMemHandle_t h;
+  SLSP_CUDA_TRY(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+  static_assert(sizeof(h) == 64, "CUDA IPC handle size");
+  std::memcpy(handle_out, &h, sizeof(h));
+  *offset_out = static_cast<int64_t>(reinterpret_cast<CUdeviceptr>(ptr) - base);
+  return SLSP_OK;
+}
+
+int slsp_ipc_open_handle(const void* handle, void** ptr_out) {
+  if (!handle || !ptr_out) return SLSP_ERR_INVALID;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  SLSP_CUDA_TRY(cudaIpcOpenMemHandle(ptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+  return SLSP_OK;
+}
+
+int slsp_ipc_close(void* ptr) {
+  if (!ptr) return SLSP_ERR_INVALID;
+  SLSP_CUDA_TRY(cudaIpcCloseMemHandle(ptr));
   return SLSP_OK;
 }
 
