@@ -138,6 +138,8 @@ def lib() -> C.CDLL:
                 "slsp_dense_gemm_config": (i32, [i32, i64, i64, i64, i32, i64, C.POINTER(GemmConfig)]),
             }
             for name, (res, args) in sigs.items():
+                if os.environ.get("SLSP_LIB") and not hasattr(L, name):
+                    continue  # an older library build under test (perf probing): only what it exports
                 fn = getattr(L, name)
                 fn.restype = res
                 fn.argtypes = args
@@ -559,15 +561,28 @@ def dense_gemm_config(dtype: int, n: int, k: int, m: int, out_mode: int = OUT_RA
     return cfg.as_dict()
 
 
+_WS: dict = {}
+_WS_MAX = 64 << 20  # the split-K slice cap (slsp_gemm_workspace_bytes bound)
+
+
 def _workspace(query, device):
-    """Split-K partial-sum slices, sized to what the chosen configuration uses
-    (nothing is allocated when the call does not split)."""
+    """Split-K workspace for a call that splits (None when it does not): one
+    buffer per device, allocated once at the library's upper bound and kept
+    for the process lifetime (no per-call allocation, and CUDA graphs that
+    captured it stay valid). Calls on one stream are ordered; concurrent
+    streams must not split at the same time."""
     cfg = GemmConfig()
     _check(query(C.byref(cfg)), "gemm_config")
     nb = int(cfg.workspace_bytes)
     if nb == 0:
         return None, 0
-    return torch.empty(nb, dtype=torch.uint8, device=device), nb
+    key = device.index if device.index is not None else torch.cuda.current_device()
+    buf = _WS.get(key)
+    if buf is None:
+        buf = _WS[key] = torch.zeros(max(nb, _WS_MAX), dtype=torch.uint8, device=device)
+    if buf.numel() < nb:
+        raise UnsupportedError(f"split-K workspace of {nb} bytes exceeds the {buf.numel()}-byte bound")
+    return buf, nb
 
 
 def _check_pairing(w: "PackedWeights", act: torch.Tensor) -> None:

@@ -1287,7 +1287,7 @@ int choose_ksplit(int tiles, int num_kb, int clusters, int cap, int64_t slice_by
   // (21 INT8 / 42 BF16 k-blocks) lose with any split at M <= 256, K = 18944
   // (111 / 222) gains 1.3-1.6x at M <= 256, ~1.1x at M = 512, and loses at
   // M = 768 (a 3-way split there cost 1.5x).
-  constexpr int kSplitCostKb = 32;
+  const int kSplitCostKb = static_cast<int>(env_knob("SLSP_GEMM_SPLITCOST", 16));
   constexpr double kSliceBytesPerKb = 1.35e6;
   int best = 1;
   double best_cost = static_cast<double>((tiles + clusters - 1) / clusters) * num_kb;
@@ -1342,7 +1342,7 @@ int run(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const 
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = slsp_host::pdl_enabled() ? 1 : 0;
+  attr[1].val.programmaticStreamSerializationAllowed = slsp_host::pdl_enabled(p.m) ? 1 : 0;
   cfg.blockDim = dim3(C::THREADS);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = s;

@@ -38,17 +38,20 @@ int status_collect(void* status_ws, cudaStream_t s, int err_code, int64_t* row, 
 // Current device must be sm_100 (B200); fails loudly otherwise.
 int require_sm100();
 
-// Programmatic dependent launch for the hot kernels (env SLSP_PDL=1 turns it on).
-bool pdl_enabled();
+// Programmatic dependent launch for the hot kernels over `rows` tokens
+// (env SLSP_PDL; see runtime.cu). Every PDL-launched kernel waits
+// (griddepcontrol.wait) before touching memory a predecessor may write.
+bool pdl_enabled(int64_t rows);
 
 // cudaLaunchKernelEx with the programmatic-stream-serialization attribute
 // (PDL) when enabled; plain launch semantics otherwise.
 template <typename... KArgs, typename... Args>
-int launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+int launch_pdl(int64_t rows, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+               Args&&... args) {
   cudaLaunchConfig_t cfg{};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled(rows) ? 1 : 0;
   cfg.gridDim = grid;
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;

@@ -536,9 +536,9 @@ template <int IN, int KIND, int L, int QPT>
 int launch_row_q(ActArgs& a, int threads, cudaStream_t s) {
   if (a.rows >= (int64_t{1} << 31)) return SLSP_ERR_UNSUPPORTED;
   if (threads <= 128 && env_row_path() != 2)
-    return slsp_host::launch_pdl(act_row1_kernel<IN, KIND, L, QPT, 128, 16>, dim3(static_cast<unsigned>(a.rows)),
+    return slsp_host::launch_pdl(a.rows, act_row1_kernel<IN, KIND, L, QPT, 128, 16>, dim3(static_cast<unsigned>(a.rows)),
                                  dim3(threads), 0, s, a);
-  return slsp_host::launch_pdl(act_row1_kernel<IN, KIND, L, QPT>, dim3(static_cast<unsigned>(a.rows)), dim3(threads),
+  return slsp_host::launch_pdl(a.rows, act_row1_kernel<IN, KIND, L, QPT>, dim3(static_cast<unsigned>(a.rows)), dim3(threads),
                                0, s, a);
 }
 

@@ -106,8 +106,14 @@ int require_sm100() {
   return SLSP_OK;
 }
 
-bool pdl_enabled() {  // off by default: measured 1% slower on the bench step
-  return knob("SLSP_PDL", 0) == 1;
+// Env SLSP_PDL: 1 on, 0 off, unset: on for calls over at most kPdlAutoRows
+// tokens — decode / moderate M, where the launch gap and the GEMM prologue
+// are a visible share (measured 1.5-2 us per lift + GEMM pair at M <= 64) —
+// and off at large M (measured 1% slower on the M=8192 bench step).
+bool pdl_enabled(int64_t rows) {
+  constexpr int64_t kPdlAutoRows = 1024;
+  const int64_t v = static_cast<int64_t>(knob("SLSP_PDL", 2));
+  return v == 1 || (v == 2 && rows <= kPdlAutoRows);
 }
 
 }  // namespace slsp_host
