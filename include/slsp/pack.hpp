@@ -4,7 +4,9 @@
 // verify_compliance and unslide are host utilities (reference pack.hpp:37-72,
 // :209-233), not on the hot path.
 
+#include <algorithm>
 #include <cstdint>
+#include <functional>
 #include <optional>
 #include <span>
 #include <string>
@@ -84,13 +86,69 @@ SlidedMatrix<T> pack_matrix(const Matrix<T>& w, const SparsityPattern& pattern, 
   return out;
 }
 
-// pack.hpp:148-167: one row.
+namespace detail {
+
+// The reference's test-only packer hooks (pack.hpp:74-122): a per-rejection
+// callback and the greedy placement with a capped window count, used to probe
+// the capacity argument. Host code: the hook observes individual placement
+// decisions, which the B200 packer (one thread per block, table-driven for
+// 6:8) does not expose. pack_row with an observer runs this; without one it
+// runs on the device like pack_matrix.
+using RejectionObserver = std::function<void(std::size_t group, int window, std::size_t src_index)>;
+
 template <typename T>
-std::vector<T> pack_row(std::span<const T> src, const WindowPlan& plan) {
+std::optional<std::size_t> greedy_pack_row(std::span<const T> src, const WindowPlan& plan, std::span<T> dst,
+                                           int window_limit, const RejectionObserver* observer = nullptr) {
+  const SparsityPattern& p = plan.pattern;
+  const std::size_t l = static_cast<std::size_t>(p.l), n = static_cast<std::size_t>(p.hw_n);
+  const std::size_t span_out = static_cast<std::size_t>(plan.window_count) * n;
+  std::fill(dst.begin(), dst.end(), T{});
+  std::optional<std::size_t> first_left;
+  for (std::size_t g = 0; g < src.size() / l; ++g) {
+    std::uint64_t taken = 0;  // bit k: source position k of this block already placed
+    for (int w = 0; w < window_limit; ++w) {
+      int placed = 0;
+      for (std::size_t d = 0; d < n; ++d) {
+        const std::size_t k = static_cast<std::size_t>(plan.window_starts[w]) + d;
+        const T v = src[g * l + k];
+        if (!is_nonzero(v) || ((taken >> k) & 1u)) continue;
+        if (placed == p.hw_m) {  // window full: the value waits for a later window
+          if (observer) (*observer)(g, w, g * l + k);
+          continue;
+        }
+        dst[g * span_out + static_cast<std::size_t>(w) * n + d] = v;
+        taken |= std::uint64_t{1} << k;
+        ++placed;
+      }
+    }
+    for (std::size_t k = 0; k < l && !first_left; ++k)
+      if (is_nonzero(src[g * l + k]) && !((taken >> k) & 1u)) first_left = g * l + k;
+  }
+  return first_left;
+}
+
+}  // namespace detail
+
+// pack.hpp:148-167: one row (on the device; with an observer, the host hook above).
+template <typename T>
+std::vector<T> pack_row(std::span<const T> src, const WindowPlan& plan,
+                        const detail::RejectionObserver* observer = nullptr) {
   const auto& p = plan.pattern;
   if (src.size() % static_cast<std::size_t>(p.l) != 0)
     throw DimensionMismatchError("row length " + std::to_string(src.size()) + " not divisible by block length " +
                                  std::to_string(p.l));
+  if (observer) {
+    for (std::size_t g = 0; g < src.size() / p.l; ++g) {
+      int nnz = 0;
+      for (int k = 0; k < p.l; ++k) nnz += is_nonzero(src[g * p.l + k]) ? 1 : 0;
+      if (nnz > p.z)
+        throw NotCompliantError("block " + std::to_string(g) + " exceeds " + std::to_string(p.z) + " nonzeros");
+    }
+    std::vector<T> dst(src.size() / p.l * plan.window_count * p.hw_n);
+    if (auto left = detail::greedy_pack_row<T>(src, plan, dst, plan.window_count, observer))
+      throw NotCompliantError("nonzero at index " + std::to_string(*left) + " left unassigned after the last window");
+    return dst;
+  }
   Matrix<T> one(1, src.size(), std::vector<T>(src.begin(), src.end()));
   try {
     return pack_matrix(one, p).data;

@@ -61,8 +61,9 @@ struct QuantizedLiftedActivation {
 namespace detail {
 template <typename T>
 constexpr int act_dtype() {
-  static_assert(std::is_same_v<T, float>, "the B200 activation kernels take float (or bf16 via the C ABI)");
-  return SLSP_DT_F32;
+  static_assert(std::is_same_v<T, float> || std::is_same_v<T, double>,
+                "the B200 activation kernels take float or double (or bf16 via the C ABI)");
+  return std::is_same_v<T, double> ? SLSP_DT_F64 : SLSP_DT_F32;
 }
 inline std::string nonfinite_message(std::int64_t row) {
   return "non-finite activation value in row " + std::to_string(row);

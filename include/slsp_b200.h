@@ -48,7 +48,8 @@ enum {
   SLSP_DT_BF16 = 1, /* bfloat16 bit patterns                          */
   SLSP_DT_E4M3 = 2, /* fp8 e4m3fn codes (fp8.hpp)                     */
   SLSP_DT_F32 = 3,
-  SLSP_DT_F64 = 4
+  SLSP_DT_F64 = 4,
+  SLSP_DT_I32 = 5   /* int32 (the reference's generic Matrix<int>)        */
 };
 
 /* Activation quantization kinds (quantize.hpp:16 QuantKind). */
@@ -293,6 +294,21 @@ SLSP_API int slsp_sparse_gemm_config(int dtype, int64_t n, int64_t kp, int64_t m
                                      slsp_gemm_config* cfg);
 SLSP_API int slsp_dense_gemm_config(int dtype, int64_t n, int64_t k, int64_t m, int out_mode, int64_t ws_bytes,
                                     slsp_gemm_config* cfg);
+
+/* gemm.hpp:142-197 generic instantiations (T = int32 -> int64 accumulators,
+ * T = float -> double) on the CUDA cores, for the drop-in's Matrix<int> /
+ * Matrix<float> calls: one thread per output element sums in the reference's
+ * left-to-right order with exact products, so results are bit-identical to
+ * the reference at any size. Not the hot path (that is tcgen05, above).
+ *   dense : w n x k, x k x m (one token per column), y n x m (int64|double)
+ *   sparse: values rows x windows x hw_m, codes same shape (one position
+ *           code per byte, gemm.hpp:49-58), lifted m x windows*hw_n (one token
+ *           per row), y rows x m; a code >= hw_n reports SLSP_ERR_MALFORMED. */
+SLSP_API int slsp_generic_dense_gemm(int dtype, const void* w, int64_t n, int64_t k, const void* x, int64_t m, void* y,
+                                     slsp_stream_t stream);
+SLSP_API int slsp_generic_sparse_gemm(int dtype, const void* values, const uint8_t* codes, int64_t rows,
+                                      int64_t windows, int hw_m, int hw_n, const void* lifted, int64_t m, void* y,
+                                      void* status_ws, int64_t* bad_row, slsp_stream_t stream);
 
 /* a15 — gemm.hpp:142-162 dense_gemm on tcgen05.mma (the speedup
  * denominator). w: n x k, act: m x k (token rows; the reference's X is k x m,

@@ -18,7 +18,7 @@ CSRC = PKG / "csrc"
 LIB = PKG / "libslsp_b200.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["runtime.cu", "pack.cu", "lift.cu", "gemm.cu"]
+SOURCES = ["runtime.cu", "pack.cu", "lift.cu", "gemm.cu", "generic.cu"]
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

@@ -113,6 +113,7 @@ inline int elem_size(int dtype) {
     case SLSP_DT_BF16:
       return 2;
     case SLSP_DT_F32:
+    case SLSP_DT_I32:
       return 4;
     case SLSP_DT_F64:
       return 8;

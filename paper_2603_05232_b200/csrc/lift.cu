@@ -662,8 +662,80 @@ int launch_act(ActArgs& a, int esz, cudaStream_t s) {
   return SLSP_OK;
 }
 
+// Double-precision rows (the drop-in's quantize_row<double> /
+// fused_quant_slide<double>): quantize.hpp:52-68 / :122-174 with T = double —
+// |x|max in double, r = qmax/absmax and codes = quantize_value(x*r) in double,
+// exactly the reference's arithmetic. One CTA per row, the row read from
+// global (L1/L2) in each pass; not a hot path.
+template <int KIND, bool LIFT>
+__global__ void __launch_bounds__(256) act_f64_kernel(ActArgs a) {
+  __shared__ double s_max[8];
+  __shared__ int s_bad[8];
+  const int tid = threadIdx.x;
+  for (int64_t row = blockIdx.x; row < a.rows; row += gridDim.x) {
+    const double* x = reinterpret_cast<const double*>(a.x) + row * a.cols;
+    double amax = 0.0;
+    int bad = 0;
+    for (int64_t k = tid; k < a.cols; k += 256) {
+      const double d = x[k];
+      bad |= !isfinite(d);
+      amax = fmax(amax, fabs(d));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+      bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+    }
+    if ((tid & 31) == 0) {
+      s_max[tid >> 5] = amax;
+      s_bad[tid >> 5] = bad;
+    }
+    __syncthreads();
+    amax = 0.0;
+    bad = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      amax = fmax(amax, s_max[w]);
+      bad |= s_bad[w];
+    }
+    __syncthreads();  // s_max / s_bad reused by the next row
+    if (bad && tid == 0 && a.status) atomicMin(a.status, static_cast<unsigned long long>(row) << 32);
+    const double qmax = KIND == K_INT8 ? 127.0 : 448.0;
+    const double r = amax == 0.0 ? 0.0 : qmax / amax;
+    if (tid == 0) a.scales[row] = amax == 0.0 ? 1.0f : __double2float_rn(amax / qmax);
+    uint8_t* dst = a.out + row * a.out_ld;
+    if constexpr (LIFT) {
+      for (int64_t j = tid; j < a.out_bytes / 4; j += 256) {  // word j = window j (quantize.hpp:155-166)
+        uint32_t word = 0;
+        if (j < a.words_real) {
+          const int64_t g = j / a.wc;
+          const int64_t b = g * a.l + 2 * (j - g * a.wc);
+#pragma unroll
+          for (int d = 0; d < 4; ++d) {
+            const int64_t k = b + d;
+            const double v = k < a.cols ? x[k] : 0.0;
+            word |= static_cast<uint32_t>(quantize_value(v * r, KIND)) << (8 * d);
+          }
+        }
+        reinterpret_cast<uint32_t*>(dst)[j] = word;
+      }
+    } else {
+      for (int64_t k = tid; k < a.out_bytes; k += 256)
+        dst[k] = k < a.cols ? static_cast<uint8_t>(quantize_value(x[k] * r, KIND)) : 0;
+    }
+  }
+}
+
 template <bool LIFT>
 int dispatch_quant(int in_dtype, int kind, ActArgs& a, cudaStream_t s) {
+  if (in_dtype == SLSP_DT_F64) {
+    if (a.rows == 0) return SLSP_OK;
+    const unsigned grid = static_cast<unsigned>(a.rows < 148 * 16 ? a.rows : 148 * 16);
+    if (kind == SLSP_QUANT_INT8) act_f64_kernel<K_INT8, LIFT><<<grid, 256, 0, s>>>(a);
+    else act_f64_kernel<K_FP8, LIFT><<<grid, 256, 0, s>>>(a);
+    SLSP_LAUNCH_CHECK();
+    return SLSP_OK;
+  }
   const int esz = in_dtype == SLSP_DT_F32 ? 4 : 2;
   if (in_dtype == SLSP_DT_F32) {
     return kind == SLSP_QUANT_INT8 ? launch_act<IN_F32, K_INT8, LIFT>(a, esz, s)
@@ -745,7 +817,8 @@ int slsp_fused_quant_slide(int in_dtype, const void* x, int64_t rows, int64_t co
   int wc = 0;
   int st = plan(z, l, &wc);  // pattern.hpp plan; hw_n == 4 by construction (quantize.hpp:125)
   if (st) return st;
-  if ((in_dtype != SLSP_DT_F32 && in_dtype != SLSP_DT_BF16) || (kind != 0 && kind != 1)) return SLSP_ERR_INVALID;
+  if ((in_dtype != SLSP_DT_F32 && in_dtype != SLSP_DT_BF16 && in_dtype != SLSP_DT_F64) || (kind != 0 && kind != 1))
+    return SLSP_ERR_INVALID;
   if (rows < 0 || cols < 0) return SLSP_ERR_INVALID;
   const int64_t groups = (cols + l - 1) / l;
   const int64_t words = groups * wc;
@@ -879,7 +952,8 @@ int slsp_quantize_rows(int in_dtype, const void* x, int64_t rows, int64_t cols, 
                        float* scales, void* status_ws, int64_t* bad_row, slsp_stream_t stream) {
   using namespace slsp_host;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if ((in_dtype != SLSP_DT_F32 && in_dtype != SLSP_DT_BF16) || (kind != 0 && kind != 1)) return SLSP_ERR_INVALID;
+  if ((in_dtype != SLSP_DT_F32 && in_dtype != SLSP_DT_BF16 && in_dtype != SLSP_DT_F64) || (kind != 0 && kind != 1))
+    return SLSP_ERR_INVALID;
   if (rows < 0 || cols < 0) return SLSP_ERR_INVALID;
   if (kpad < cols || kpad % 16 != 0) return SLSP_ERR_DIMENSION;
   int st;

@@ -23,7 +23,7 @@ template <int ESZ>
 SLSP_DEVINL bool nonzero_bits(uint64_t bits, int dtype) {
   if constexpr (ESZ == 1) return dtype == SLSP_DT_E4M3 ? (bits & 0x7Fu) != 0 : (bits & 0xFFu) != 0;
   if constexpr (ESZ == 2) return (bits & 0x7FFFu) != 0;
-  if constexpr (ESZ == 4) return (bits & 0x7FFFFFFFu) != 0;
+  if constexpr (ESZ == 4) return dtype == SLSP_DT_I32 ? (bits & 0xFFFFFFFFu) != 0 : (bits & 0x7FFFFFFFu) != 0;
   return (bits & 0x7FFFFFFFFFFFFFFFull) != 0;
 }
 
@@ -215,7 +215,10 @@ SLSP_DEVINL double magnitude(uint64_t bits, int dtype) {
     return fabs(static_cast<double>(static_cast<int8_t>(bits)));
   }
   if constexpr (ESZ == 2) return fabs(static_cast<double>(__uint_as_float(static_cast<uint32_t>(bits) << 16)));
-  if constexpr (ESZ == 4) return fabs(static_cast<double>(__uint_as_float(static_cast<uint32_t>(bits))));
+  if constexpr (ESZ == 4) {
+    if (dtype == SLSP_DT_I32) return fabs(static_cast<double>(static_cast<int32_t>(static_cast<uint32_t>(bits))));
+    return fabs(static_cast<double>(__uint_as_float(static_cast<uint32_t>(bits))));
+  }
   return fabs(__longlong_as_double(static_cast<long long>(bits)));
 }
 
