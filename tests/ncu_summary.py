@@ -30,7 +30,27 @@ METRICS = [
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput %"),
     ("gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed", "memory throughput %"),
     ("smsp__inst_executed.sum", "instructions"),
+    ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "tensor pipe active % (non-realtime)"),
+    ("sm__inst_executed_pipe_uma.avg.pct_of_peak_sustained_active", "UMA (tcgen05) pipe inst % of peak"),
+    ("sm__inst_executed_pipe_tma.avg.pct_of_peak_sustained_active", "TMA pipe inst % of peak"),
 ]
+
+
+def grep(paths, pattern):
+    """Every raw metric whose name matches `pattern` (regex), per capture."""
+    import re
+
+    rx = re.compile(pattern)
+    for path in paths:
+        raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True,
+                             check=True).stdout
+        rows = list(csv.reader(io.StringIO(raw)))
+        head, units = rows[0], rows[1]
+        for r in rows[2:]:
+            print(f"== {path.split('/')[-1]}: {r[head.index('Kernel Name')][:100]}")
+            for i, h in enumerate(head):
+                if rx.search(h):
+                    print(f"   {h:90s} {r[i]:>16s} {units[i]}")
 
 
 def full(paths):
@@ -70,5 +90,7 @@ def launches(path):
 if __name__ == "__main__":
     if sys.argv[1] == "--launches":
         launches(sys.argv[2])
+    elif sys.argv[1] == "--grep":
+        grep(sys.argv[3:], sys.argv[2])
     else:
         full(sys.argv[1:])
