@@ -52,8 +52,11 @@ constexpr int epi_cols(int msub, int bn, int out) {
 }
 
 template <bool SPARSE_, MmaKind KIND_, int BN_, int STAGES_, int OUT_, int MSUB_ = 1, int LIFT_ = 0, int KH_ = 0,
-          int NPAIR_ = 1>
+          int NPAIR_ = 1, int AMAX_ = 0>
 struct Cfg {
+  // §8f #3: the token |y|max fold compiled in (slsp_sparse_gemm_amax only; the
+  // plain kernels carry none of its registers)
+  static constexpr bool AMAX = AMAX_ != 0;
   static constexpr bool SPARSE = SPARSE_;
   static constexpr MmaKind KIND = KIND_;
   static constexpr int BN = BN_;          // tokens per pair tile (MMA N)
@@ -148,7 +151,7 @@ struct Cfg {
   // §8f #3 token |y|max fold (BF16 outputs): a per-CTA [2][BN] merge buffer
   // where it costs no ring stage; otherwise the fold goes to global atomics
   // per warp
-  static constexpr int AMAX_CAND = SPARSE && OUT != SLSP_OUT_RAW_NM ? 2 * BN * 4 : 0;
+  static constexpr int AMAX_CAND = AMAX && SPARSE && OUT != SLSP_OUT_RAW_NM ? 2 * BN * 4 : 0;
   static constexpr bool AMAX_SM =
       AMAX_CAND > 0 && (227 * 1024 - FIXED_SMEM0 - AMAX_CAND) / (STAGE_TX + 16) >= (FIT0 < 8 ? FIT0 : 8);
   static constexpr int AMAX_BYTES = AMAX_SM ? AMAX_CAND : 0;
@@ -452,7 +455,7 @@ SLSP_DEVINL void epilogue_chunk(const Params& p, const CUtensorMap* tmOut, uint8
       w[i] = pack_bf16(lo, hi);
     }
   }
-  if constexpr (C::OUT != SLSP_OUT_RAW_NM)
+  if constexpr (C::AMAX && C::OUT != SLSP_OUT_RAW_NM)
     if (p.amax) fold_token_amax<NW>(p, w, t0, amax_sm, c0);
   if (p.debug & kDbgNoStore) return;
 
@@ -1056,7 +1059,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         tc_fence_after();
       }
       drain(1, sc1, pk1);
-      if (p.amax) {  // §8f #3: both subtiles' rows, then across lanes and warps
+      if (C::AMAX && p.amax) {  // §8f #3: both subtiles' rows, then across lanes and warps
         const uint32_t sm = C::AMAX_SM ? smem_u32(smem + C::OFF_AMAX) + (it & 1) * C::BN * 4 : 0u;
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
@@ -1145,7 +1148,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[C::MSUB == 2 ? h : acc]), lead));
       }
       if constexpr (C::AMAX_SM)
-        if (p.amax)
+        if (C::AMAX && p.amax)
           fold_flush<C::BN, C::EPI_WARPS * 32>(p, reinterpret_cast<uint32_t*>(smem + C::OFF_AMAX) + (it & 1) * C::BN,
                                                static_cast<int64_t>(nt) * C::BN, warp == 2);
     }
@@ -1400,6 +1403,25 @@ int run(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const 
   return SLSP_OK;
 }
 
+// The amax-folding instantiations (slsp_sparse_gemm_amax): BF16 outputs, no
+// half k-stages, no weight multicast, no in-SM lifting.
+template <MmaKind K, int BN>
+int run_amax(int out_mode, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const CUtensorMap& o,
+             const Params& p, cudaStream_t s, uint32_t msub, slsp_gemm_config* q) {
+  constexpr bool two_sub = BN >= 128 && BN <= 224;
+  if (out_mode == SLSP_OUT_BF16_NM) {
+    if constexpr (two_sub)
+      if (msub == 2) return run<Cfg<true, K, BN, 0, SLSP_OUT_BF16_NM, 2, 0, 0, 1, 1>>(a, b, e, o, p, s, q);
+    return run<Cfg<true, K, BN, 0, SLSP_OUT_BF16_NM, 1, 0, 0, 1, 1>>(a, b, e, o, p, s, q);
+  }
+  if (out_mode == SLSP_OUT_BF16_MN) {
+    if constexpr (two_sub)
+      if (msub == 2) return run<Cfg<true, K, BN, 0, SLSP_OUT_BF16_MN, 2, 0, 0, 1, 1>>(a, b, e, o, p, s, q);
+    return run<Cfg<true, K, BN, 0, SLSP_OUT_BF16_MN, 1, 0, 0, 1, 1>>(a, b, e, o, p, s, q);
+  }
+  return SLSP_ERR_INVALID;
+}
+
 template <bool SPARSE, MmaKind K, int BN, int MSUB, int LIFT, int KH, int NPAIR = 1>
 int run_out_cl(int out_mode, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const CUtensorMap& o,
                const Params& p, cudaStream_t s, slsp_gemm_config* q) {
@@ -1544,7 +1566,7 @@ int sparse_entry(int dtype, const void* values, const uint8_t* meta, int64_t n, 
   // half k-stages: the two-subtile BF16 [N][M] config (off by default), and
   // every one-subtile 8-bit config below the large-M regime (on: a 7-8
   // stage ring instead of 3-4 for the weight-stream-heavy moderate M)
-  const uint32_t kh = !LIFT && !decode && esz == 1 &&
+  const uint32_t kh = !LIFT && !decode && esz == 1 && !tok_amax &&
                               ((msub == 2 && out_mode == SLSP_OUT_BF16_NM &&
                                 env_knob("SLSP_GEMM_KHALF", kSparseKHalf)) ||
                                (msub == 1 && m <= kBn256MaxM && env_knob("SLSP_GEMM_KHALF1", kSparseKHalf1)))
@@ -1584,6 +1606,18 @@ int sparse_entry(int dtype, const void* values, const uint8_t* meta, int64_t n, 
   p.pf_at = static_cast<int>(env_knob("SLSP_GEMM_PFAT", 8));
   constexpr int L = LIFT ? 1 : 0;
   if constexpr (!LIFT) {
+    if (tok_amax) {  // the fold variants: 8-bit kinds (the next layer quantizes), no half k-stages
+      if (dtype == SLSP_DT_BF16) return SLSP_ERR_UNSUPPORTED;
+      const bool i8 = dtype == SLSP_DT_I8;
+      if (decode)
+        return i8 ? run_amax<MmaKind::I8, kDecodeBN>(out_mode, ta, tb, te, to, p, s, 1, q)
+                  : run_amax<MmaKind::F8, kDecodeBN>(out_mode, ta, tb, te, to, p, s, 1, q);
+      if (wide)
+        return i8 ? run_amax<MmaKind::I8, kSparseBN256>(out_mode, ta, tb, te, to, p, s, 1, q)
+                  : run_amax<MmaKind::F8, kSparseBN256>(out_mode, ta, tb, te, to, p, s, 1, q);
+      return i8 ? run_amax<MmaKind::I8, kSparseBN>(out_mode, ta, tb, te, to, p, s, msub, q)
+                : run_amax<MmaKind::F8, kSparseBN>(out_mode, ta, tb, te, to, p, s, msub, q);
+    }
     if (decode) {
       if (dtype == SLSP_DT_I8) return run_out<true, MmaKind::I8, kDecodeBN>(out_mode, ta, tb, te, to, p, s, 1, 0, q);
       if (dtype == SLSP_DT_BF16)

@@ -276,14 +276,14 @@ __device__ __noinline__ uint32_t quant4_bf16_int8_slow(uint32_t wa, uint32_t wb,
 // quant_int8_fast for 4 BF16 elements (two bf16x2 words) with packed f32x2
 // math: byte d of the result = code of element d. Any element within 3e-5 of
 // a half-integer sends all four to the exact FP64 path (out of line: rare).
-SLSP_DEVINL uint32_t quant4_bf16_int8(uint32_t wa, uint32_t wb, float r32, double r) {
+SLSP_DEVINL uint32_t quant4_bf16_int8(uint32_t wa, uint32_t wb, float r32, double r, bool exact_r = false) {
   const float2 M = make_float2(12582912.0f, 12582912.0f), R = make_float2(r32, r32);
   const float2 y0 = fmul2_rn(make_float2(__uint_as_float(wa << 16), __uint_as_float(wa & 0xFFFF0000u)), R);
   const float2 y1 = fmul2_rn(make_float2(__uint_as_float(wb << 16), __uint_as_float(wb & 0xFFFF0000u)), R);
   const float2 t0 = fadd2_rn(y0, M), t1 = fadd2_rn(y1, M);
   const float2 f0 = fsub2_rn(y0, fsub2_rn(t0, M)), f1 = fsub2_rn(y1, fsub2_rn(t1, M));
   const float m = fmaxf(fmaxf(fabsf(f0.x), fabsf(f0.y)), fmaxf(fabsf(f1.x), fabsf(f1.y)));
-  if (m >= 0.49997f) return quant4_bf16_int8_slow(wa, wb, r);
+  if (!exact_r && m >= 0.49997f) return quant4_bf16_int8_slow(wa, wb, r);
   return __byte_perm(__byte_perm(__float_as_uint(t0.x), __float_as_uint(t0.y), 0x0040),
                      __byte_perm(__float_as_uint(t1.x), __float_as_uint(t1.y), 0x0040), 0x5410);
 }
@@ -292,7 +292,7 @@ SLSP_DEVINL uint32_t quant4_bf16_int8(uint32_t wa, uint32_t wb, float r32, doubl
 // for the quad's groups): quantize every source element once, then window w
 // of block g = bytes [g*L + 2w, +4) of the quad's codes.
 template <int IN, int KIND, int L>
-SLSP_DEVINL void emit_quad(const uint4 (&v)[WarpGeom<IN, KIND, L>::IN_VEC], float r32, double r,
+SLSP_DEVINL void emit_quad(const uint4 (&v)[WarpGeom<IN, KIND, L>::IN_VEC], float r32, double r, bool exact_r,
                            uint32_t (&o)[WarpGeom<IN, KIND, L>::OUT_VEC * 4]) {
   using G = WarpGeom<IN, KIND, L>;
       if constexpr (KIND != K_NONE) {
@@ -302,7 +302,7 @@ SLSP_DEVINL void emit_quad(const uint4 (&v)[WarpGeom<IN, KIND, L>::IN_VEC], floa
         for (int i = 0; i < G::ELEMS / 4; ++i) {
           if constexpr (KIND == K_INT8 && IN == IN_BF16) {
             const uint32_t* iw = reinterpret_cast<const uint32_t*>(v);
-            qw[i] = quant4_bf16_int8(iw[2 * i], iw[2 * i + 1], r32, r);
+            qw[i] = quant4_bf16_int8(iw[2 * i], iw[2 * i + 1], r32, r, exact_r);
           } else {
             uint32_t b[4];
 #pragma unroll
@@ -352,6 +352,7 @@ __global__ void __launch_bounds__(256) act_warp_kernel(ActArgs a) {
     const uint4* src = reinterpret_cast<const uint4*>(a.x + row * a.cols * G::ESZ);
     double r = 0.0;
     float r32 = 0.f;
+    bool exact_r = false;
     if constexpr (KIND != K_NONE) {
       float amax = 0.f;
       int bad = 0;
@@ -401,6 +402,10 @@ __global__ void __launch_bounds__(256) act_warp_kernel(ActArgs a) {
       const double absmax = static_cast<double>(amax);
       r = absmax == 0.0 ? 0.0 : qmax / absmax;
       r32 = __double2float_rn(r);
+      // r exactly representable with <= 16 significant bits (e.g. absmax a power
+      // of two): every bf16 x times r32 is exact in fp32, ties included
+      exact_r = IN == IN_BF16 && KIND == K_INT8 && r32 != 0.f &&
+                fmaf(r32, static_cast<float>(absmax), -127.0f) == 0.f && (__float_as_uint(r32) & 0xFFu) == 0u;
       if (lane == 0) a.scales[row] = absmax == 0.0 ? 1.0f : __double2float_rn(absmax / qmax);
     }
 #pragma unroll 2
@@ -409,7 +414,7 @@ __global__ void __launch_bounds__(256) act_warp_kernel(ActArgs a) {
 #pragma unroll
       for (int i = 0; i < G::IN_VEC; ++i) v[i] = __ldg(src + q * G::IN_VEC + i);
       uint32_t o[G::OUT_VEC * 4];
-      emit_quad<IN, KIND, L>(v, r32, r, o);
+      emit_quad<IN, KIND, L>(v, r32, r, exact_r, o);
 #pragma unroll
       for (int i = 0; i < G::OUT_VEC; ++i)
         store_out_vec(a, row, q * G::OUT_VEC + i, make_uint4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]));
@@ -448,6 +453,7 @@ SLSP_DEVINL void row_emit(const ActArgs& a, int64_t row, int nquads, float* s_ma
   const int nthr = blockDim.x;
   double r = 0.0;
   float r32 = 0.f;
+  bool exact_r = false;
   if constexpr (KIND != K_NONE) {
     float amax;
     if (a.amax_in) {
@@ -501,6 +507,10 @@ SLSP_DEVINL void row_emit(const ActArgs& a, int64_t row, int nquads, float* s_ma
     const double absmax = static_cast<double>(amax);
     r = absmax == 0.0 ? 0.0 : qmax / absmax;
     r32 = __double2float_rn(r);
+    // r exactly representable with <= 16 significant bits (e.g. absmax a power
+    // of two): every bf16 x times r32 is exact in fp32, ties included
+    exact_r = IN == IN_BF16 && KIND == K_INT8 && r32 != 0.f &&
+              fmaf(r32, static_cast<float>(absmax), -127.0f) == 0.f && (__float_as_uint(r32) & 0xFFu) == 0u;
     if (tid == 0) a.scales[row] = absmax == 0.0 ? 1.0f : __double2float_rn(absmax / qmax);
   }
 #pragma unroll
@@ -508,7 +518,7 @@ SLSP_DEVINL void row_emit(const ActArgs& a, int64_t row, int nquads, float* s_ma
     const int q = tid + j * nthr;
     if (q >= nquads) break;
     uint32_t o[G::OUT_VEC * 4];
-    emit_quad<IN, KIND, L>(v[j], r32, r, o);
+    emit_quad<IN, KIND, L>(v[j], r32, r, exact_r, o);
 #pragma unroll
     for (int i = 0; i < G::OUT_VEC; ++i)
       store_out_vec(a, row, q * G::OUT_VEC + i, make_uint4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]));
@@ -542,148 +552,12 @@ int launch_row_q(ActArgs& a, int threads, cudaStream_t s) {
                                0, s, a);
 }
 
-// ---------------------------------------------------------------------------
-// Hot path, BF16 -> INT8 (fused_quant_slide 6:8 and quantize_rows), written
-// for instruction economy (the row-resident kernel above issued ~2.2k warp
-// instructions per 3584-wide row and was issue-bound at 56-60% of HBM): one
-// CTA per row, each thread one or more 32-element units held in registers.
-//  * |x|max on the bf16 bit patterns: max of (w & 0x7FFF7FFF) per halfword
-//    (for non-negative bf16 the bit order is the value order; NaN > Inf > any
-//    finite, so the row is non-finite iff the max >= 0x7F80); warp shuffles +
-//    one smem hop.
-//  * r32 = 127/absmax in fp32 (__fdiv_rn). It is within 2^-24 (relative) of
-//    the reference's double r (quantize.hpp:151), so y = x*r32 is within
-//    1.2e-5 of the reference's x*r for |y| <= 127.5: rounding y with the
-//    1.5*2^23 magic constant is exact unless y is within 3e-5 of a
-//    half-integer; any such element sends its whole 32-element unit to the
-//    FP64 path (out of line; double r computed there).
-//  * codes of 4 consecutive elements are gathered into one word (byte d =
-//    element d); 6:8 windows of a block with code words A (c0-c3), B (c4-c7):
-//    W0 = A, W1 = bytes c2-c5 = PRMT(A, B), W2 = B (quantize.hpp:155-166).
-template <bool LIFT, int UPT, int MAXT = 1024, int MINB = 1>
-__global__ void __launch_bounds__(MAXT, MINB) lift_bf16_i8_kernel(ActArgs a) {
-  __shared__ uint32_t s_max[32];
-  const int tid = threadIdx.x, nthr = blockDim.x;
-  const int64_t row = blockIdx.x;
-  const int units = static_cast<int>(a.cols >> 5);
-  pdl_wait();  // the activations may come from the previous kernel (PDL launch)
-  pdl_trigger();
-  const uint4* src = reinterpret_cast<const uint4*>(a.x + row * a.cols * 2);
-  uint4 v[UPT][4];
-#pragma unroll
-  for (int j = 0; j < UPT; ++j) {
-    const int u = tid + j * nthr;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) v[j][i] = u < units ? __ldg(src + u * 4 + i) : make_uint4(0, 0, 0, 0);
-  }
-  uint32_t mbits;  // max |x| as bf16 bits
-  if (a.amax_in) {
-    mbits = __float_as_uint(a.amax_in[row]) >> 16;  // upstream |x|max of the bf16 values: exact bf16
-    if (isnan(a.amax_in[row])) mbits = 0x7FC0u;
-  } else {
-    uint32_t m2 = 0;
-#pragma unroll
-    for (int j = 0; j < UPT; ++j)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        m2 = __vmaxu2(m2, v[j][i].x & 0x7FFF7FFFu);
-        m2 = __vmaxu2(m2, v[j][i].y & 0x7FFF7FFFu);
-        m2 = __vmaxu2(m2, v[j][i].z & 0x7FFF7FFFu);
-        m2 = __vmaxu2(m2, v[j][i].w & 0x7FFF7FFFu);
-      }
-    uint32_t m = max(m2 & 0xFFFFu, m2 >> 16);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((tid & 31) == 0) s_max[tid >> 5] = m;
-    __syncthreads();
-    m = 0;
-    for (int w = 0; w < (nthr >> 5); ++w) m = max(m, s_max[w]);
-    mbits = m;
-  }
-  const float amax = __uint_as_float(mbits << 16);
-  if (mbits >= 0x7F80u && tid == 0 && a.status) atomicMin(a.status, static_cast<unsigned long long>(row) << 32);
-  const float r32 = mbits == 0 ? 0.f : __fdiv_rn(127.0f, amax);
-  if (tid == 0) a.scales[row] = mbits == 0 ? 1.0f : __double2float_rn(static_cast<double>(amax) / 127.0);
-  // Exactly representable r with <= 16 significant bits (e.g. absmax a power
-  // of two, r = 127 * 2^-e): every bf16 x (8 bits) times r32 is exact in fp32
-  // and equals the reference's double product, ties included — the rounding
-  // needs no near-tie check (fma residual 0 <=> r32 * amax == 127 exactly).
-  const bool exact_r = r32 != 0.f && fmaf(r32, amax, -127.0f) == 0.f && (__float_as_uint(r32) & 0xFFu) == 0u;
-  const float2 M = make_float2(12582912.0f, 12582912.0f), R = make_float2(r32, r32);
-#pragma unroll
-  for (int j = 0; j < UPT; ++j) {
-    const int u = tid + j * nthr;
-    if (u >= units) break;
-    const uint32_t* w = reinterpret_cast<const uint32_t*>(v[j]);
-    uint32_t cw[8];
-    float fm = 0.f;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const uint32_t wa = w[2 * i], wb = w[2 * i + 1];
-      const float2 y0 = fmul2_rn(make_float2(__uint_as_float(wa << 16), __uint_as_float(wa & 0xFFFF0000u)), R);
-      const float2 y1 = fmul2_rn(make_float2(__uint_as_float(wb << 16), __uint_as_float(wb & 0xFFFF0000u)), R);
-      const float2 t0 = fadd2_rn(y0, M), t1 = fadd2_rn(y1, M);
-      const float2 f0 = fsub2_rn(y0, fsub2_rn(t0, M)), f1 = fsub2_rn(y1, fsub2_rn(t1, M));
-      fm = fmaxf(fm, fmaxf(fmaxf(fabsf(f0.x), fabsf(f0.y)), fmaxf(fabsf(f1.x), fabsf(f1.y))));
-      cw[i] = __byte_perm(__byte_perm(__float_as_uint(t0.x), __float_as_uint(t0.y), 0x0040),
-                          __byte_perm(__float_as_uint(t1.x), __float_as_uint(t1.y), 0x0040), 0x5410);
-    }
-    if (!exact_r && fm >= 0.49997f) {  // a near-tie: the whole unit in FP64 with the reference's r
-      const double r = static_cast<double>(127.0) / static_cast<double>(amax);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) cw[i] = quant4_bf16_int8_slow(w[2 * i], w[2 * i + 1], r);  // (unrolled: cw stays in registers)
-    }
-    if constexpr (LIFT) {
-      uint32_t o[12];
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        o[3 * b] = cw[2 * b];
-        o[3 * b + 1] = __byte_perm(cw[2 * b], cw[2 * b + 1], 0x5432);
-        o[3 * b + 2] = cw[2 * b + 1];
-      }
-#pragma unroll
-      for (int i = 0; i < 3; ++i)
-        store_out_vec(a, row, u * 3 + i, make_uint4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]));
-    } else {
-#pragma unroll
-      for (int i = 0; i < 2; ++i)
-        store_out_vec(a, row, u * 2 + i, make_uint4(cw[4 * i], cw[4 * i + 1], cw[4 * i + 2], cw[4 * i + 3]));
-    }
-  }
-  const int out_vecs = static_cast<int>(a.out_bytes >> 4);
-  for (int i = units * (LIFT ? 3 : 2) + tid; i < out_vecs; i += nthr) store_out_vec(a, row, i, make_uint4(0, 0, 0, 0));
-}
-
-template <bool LIFT>
-int launch_bf16_i8(ActArgs& a, cudaStream_t s) {
-  const int64_t units = a.cols >> 5;
-  const int upt = units <= 256 ? 1 : units <= 1024 ? 2 : 4;
-  if (units > 1024 * upt || units == 0) return -1;
-  const int threads = static_cast<int>(((units + upt - 1) / upt + 31) / 32 * 32);
-  const dim3 grid(static_cast<unsigned>(a.rows));
-  if (upt == 1 && threads <= 128)  // short rows: 16 resident CTAs per SM (<= 32 registers)
-    return slsp_host::launch_pdl(a.rows, lift_bf16_i8_kernel<LIFT, 1, 128, 16>, grid, dim3(threads), 0, s, a);
-  if (upt == 1) return slsp_host::launch_pdl(a.rows, lift_bf16_i8_kernel<LIFT, 1>, grid, dim3(threads), 0, s, a);
-  if (upt == 2) return slsp_host::launch_pdl(a.rows, lift_bf16_i8_kernel<LIFT, 2>, grid, dim3(threads), 0, s, a);
-  return slsp_host::launch_pdl(a.rows, lift_bf16_i8_kernel<LIFT, 4>, grid, dim3(threads), 0, s, a);
-}
-
 // Row-resident launch when the row fits (<= 4 quads per thread, <= 1024
 // threads); returns 0 when the caller should use the warp path.
 template <int IN, int KIND, int L>
 int launch_row(ActArgs& a, cudaStream_t s, int* st) {
   // BF16 input, 6:8 lift or quantize_rows (the hot path); the rest use the warp path
   if constexpr (IN != IN_BF16 || (L != 8 && L != 4)) return 0;
-  if constexpr (KIND == K_INT8) {
-    // the instruction-lean BF16 -> INT8 kernel (env SLSP_LIFT_ROW=3: the older row kernel, A/B probing)
-    if (a.cols % 32 == 0 && a.rows < (int64_t{1} << 31) && env_row_path() != 3) {
-      const int r = launch_bf16_i8<L == 8>(a, s);
-      if (r >= 0) {
-        *st = r;
-        return 1;
-      }
-    }
-  }
   using G = WarpGeom<IN, KIND, L>;
   const int64_t nquads = a.cols / G::ELEMS;
   // >= 64 input bytes per thread in flight (a quad is 4L elements), <= 1024 threads

@@ -28,8 +28,11 @@ elif mode.startswith("dec"):
     lifted = slsp.lift_rows(x, 6, 8, kp=pw.kp)
     fn = (lambda: slsp.sparse_gemm(pw, lifted)) if mode == "dec_sparse" else (lambda: slsp.dense_gemm(w, x))
 elif mode.startswith("lift"):
-    m = int(mode[len("lift_m"):])
-    x = (torch.rand(m, 3584, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    m = int(mode.split("_m")[1])
+    if mode.startswith("liftg"):  # gaussian rows with per-row scales (absmax not a power of two)
+        x = (torch.randn(m, 3584, device="cuda", generator=g) * (torch.rand(m, 1, device="cuda", generator=g) * 3 + 0.1)).to(torch.bfloat16)
+    else:
+        x = (torch.rand(m, 3584, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
     pay, st = slsp.fused_quant_slide(x, 6, 8)
     fn = lambda: slsp.fused_quant_slide(x, 6, 8, check=False, payload=pay, scales=st)  # noqa: E731
 elif mode == "chain_amax":
