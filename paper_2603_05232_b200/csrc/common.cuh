@@ -375,6 +375,56 @@ SLSP_DEVINL void tmem_ld_cols(uint32_t taddr, uint32_t (&r)[N]) {
 
 SLSP_DEVINL void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// tcgen05.ld.16x256b.x1: 16 TMEM lanes x 8 columns; thread T receives
+// r0 = (lane T/4, col 2(T%4)), r1 = (lane T/4, col 2(T%4)+1),
+// r2 = (lane 8+T/4, col 2(T%4)), r3 = (lane 8+T/4, col 2(T%4)+1) — measured
+// (tests/micro/tmem_layout.cu); the mma.sync C-fragment layout.
+SLSP_DEVINL void tmem_ld_16x256b_x1(uint32_t taddr, uint32_t (&r)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.16x256b.x1.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+}
+// .x2: two consecutive 8-column blocks, registers [4i, 4i+4) = block i (measured)
+SLSP_DEVINL void tmem_ld_16x256b_x2(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.16x256b.x2.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+SLSP_DEVINL void tmem_ld_wait_regs16(uint32_t (&a)[8], uint32_t (&b)[8]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(a[0]), "+r"(a[1]), "+r"(a[2]), "+r"(a[3]), "+r"(a[4]), "+r"(a[5]), "+r"(a[6]), "+r"(a[7]),
+                 "+r"(b[0]), "+r"(b[1]), "+r"(b[2]), "+r"(b[3]), "+r"(b[4]), "+r"(b[5]), "+r"(b[6]), "+r"(b[7])
+               :
+               : "memory");
+}
+SLSP_DEVINL void tmem_ld_wait_regs8(uint32_t (&a)[4], uint32_t (&b)[4]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(a[0]), "+r"(a[1]), "+r"(a[2]), "+r"(a[3]), "+r"(b[0]), "+r"(b[1]), "+r"(b[2]), "+r"(b[3])
+               :
+               : "memory");
+}
+
+// stmatrix.m8n8.x4.trans: stored row r of matrix m (16 bytes at the address
+// lane 8m + r supplies) = for j = 0..7 the (r & 1) half of register m of
+// thread 4j + r/2 (measured, tests/micro/tmem_layout.cu). With register m of
+// thread T = (feature 8m + T/4: tokens 2(T%4), 2(T%4)+1) that is row = token r,
+// 8 consecutive features — the transpose the token-major epilogue needs.
+// ldmatrix.m8n8.x4 (no transpose): register i of thread T = (row T/4, cols
+// 2(T%4), 2(T%4)+1) of matrix i, whose row j is read at the address lane 8i+j
+// supplies (16 bytes = 8 b16).
+SLSP_DEVINL void ldmatrix_x4(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr)
+               : "memory");
+}
+
+SLSP_DEVINL void stmatrix_x4_trans(uint32_t addr, uint32_t r0, uint32_t r1, uint32_t r2, uint32_t r3) {
+  asm volatile("stmatrix.sync.aligned.m8n8.x4.trans.shared.b16 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(r0),
+               "r"(r1), "r"(r2), "r"(r3)
+               : "memory");
+}
+
 // wait::ld that also orders every later use of r after the wait (the
 // registers of an in-flight tcgen05.ld are read-write operands of the wait).
 SLSP_DEVINL void tmem_ld_wait_regs(uint32_t (&r)[16]) {
@@ -397,6 +447,12 @@ SLSP_DEVINL void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;
 SLSP_DEVINL uint4 ld_shared_u4(uint32_t addr) {
   uint4 v;
   asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+
+SLSP_DEVINL float2 ld_shared_f2(uint32_t addr) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
   return v;
 }
 

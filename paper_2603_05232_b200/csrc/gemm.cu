@@ -48,7 +48,7 @@ constexpr uint32_t kDefaultHints = kHintBLast | kHintOutFirst;
 constexpr int epi_cols(int msub, int bn, int out) {
   // msub 2: the register-staged BF16 [N][M] epilogue stores 32-column boxes;
   // the generic path drains 16-column chunks
-  return msub == 2 ? (out == SLSP_OUT_BF16_NM ? 32 : 16) : (out == SLSP_OUT_RAW_NM || bn % 64 != 0) ? 32 : 64;
+  return msub == 2 ? (out != SLSP_OUT_RAW_NM ? 32 : 16) : (out == SLSP_OUT_RAW_NM || bn % 64 != 0) ? 32 : 64;
 }
 
 template <bool SPARSE_, MmaKind KIND_, int BN_, int STAGES_, int OUT_, int MSUB_ = 1, int LIFT_ = 0, int KH_ = 0,
@@ -141,7 +141,9 @@ struct Cfg {
   // MSUB=2 with BF16 [N][M] output: register-staged epilogue (each subtile is
   // dequantised into registers and its TMEM released before any store), no
   // smem staging.
-  static constexpr bool REG_EPI = MSUB == 2 && OUT == SLSP_OUT_BF16_NM;
+  // (token-major [M][N] output too: the same drain, the staged boxes
+  // transposed in shared memory before the TMA store)
+  static constexpr bool REG_EPI = MSUB == 2 && OUT != SLSP_OUT_RAW_NM && !(LIFT && OUT == SLSP_OUT_BF16_MN);
   static constexpr int H0 = (BN / 2 + 31) / 32 * 32;  // REG: columns of the first warp of a lane quarter
   // REG: s_tok slice + one 32x32 BF16 staging box per warp
   static constexpr int EPI_WARP = REG_EPI ? H0 * 4 + 32 * 64 : EPI_BUFS * EPI_BUF;
@@ -1027,10 +1029,31 @@ __global__ void __launch_bounds__(C::THREADS, 1)
               const int o = 4 * (j & 1);
               st_shared_v4(sb + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4), w[o], w[o + 1], w[o + 2], w[o + 3]);
             }
+            if constexpr (C::OUT == SLSP_OUT_BF16_MN) {
+              // transpose the [32 features][32 tokens] box in place into the
+              // [M][N] map's [32 tokens][32 features] box (64-byte rows, 64B
+              // swizzle): ldmatrix reads 8x8 blocks with features as rows,
+              // stmatrix.trans writes them back with tokens as rows
+              __syncwarp();
+              uint32_t q[4][4];
+#pragma unroll
+              for (int tb = 0; tb < 4; ++tb)  // token block: 8 tokens = one 16-byte chunk of a feature row
+                ldmatrix_x4(sb + lane * 64 + ((tb ^ ((lane >> 1) & 3)) << 4), q[tb]);
+              __syncwarp();
+#pragma unroll
+              for (int tb = 0; tb < 4; ++tb) {
+                const uint32_t tr = tb * 8 + (lane & 7);  // token row written by this lane, feature chunk lane / 8
+                stmatrix_x4_trans(sb + tr * 64 + (((lane >> 3) ^ ((tr >> 1) & 3)) << 4), q[tb][0], q[tb][1], q[tb][2],
+                                  q[tb][3]);
+              }
+            }
             fence_async_smem();
             __syncwarp();
             if (lane == 0) {
-              tma_store_2d_hint(&tmOut, stage, static_cast<int>(t0), static_cast<int>(rq), pol);
+              if constexpr (C::OUT == SLSP_OUT_BF16_MN)
+                tma_store_2d_hint(&tmOut, stage, static_cast<int>(rq), static_cast<int>(t0), pol);
+              else
+                tma_store_2d_hint(&tmOut, stage, static_cast<int>(t0), static_cast<int>(rq), pol);
               bulk_commit();
             }
           }
@@ -1038,6 +1061,18 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         }
         const int64_t row = row0 + h * 256;
         if (row >= p.n) return;
+        if constexpr (C::OUT == SLSP_OUT_BF16_MN) {  // direct 2-byte stores, coalesced across the lanes' features
+          uint16_t* out16 = reinterpret_cast<uint16_t*>(p.out);
+#pragma unroll
+          for (int c = 0; c < NCH; ++c)
+            if (c < nch)
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                const int64_t t = tcol0 + 16 * c + i;
+                if (t < p.m) out16[t * p.ldo + row] = static_cast<uint16_t>(pk[c][i >> 1] >> (16 * (i & 1)));
+              }
+          return;
+        }
         uint8_t* dst_row = reinterpret_cast<uint8_t*>(p.out) + (row * p.ldo + tcol0) * 2;
         if (p.direct_vec == 2 && tcol0 + ncols <= p.m) {
 #pragma unroll
