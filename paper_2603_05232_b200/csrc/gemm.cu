@@ -990,7 +990,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       tc_fence_after();
       if (warp == 2 && lane == 0) SLSP_TRACE(it, 3);
 
-      auto drain = [&](int h, float sc, uint32_t (&pk)[NCH][8]) {
+      auto drain = [&](int h, float sc, uint32_t (&pk)[NCH][8]) __attribute__((always_inline)) {
         const uint32_t t_base = tmem + ((quarter * 32) << 16) + h * C::ACC_COLS + half * C::H0;
         uint32_t r[2][16];
         tmem_ld_32x32b_x16(t_base, r[0]);
@@ -1009,7 +1009,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[h]), lead));
         if (warp == 2 && lane == 0) SLSP_TRACE(it, 4 + 2 * h);
       };
-      auto store = [&](int h, const uint32_t (&pk)[NCH][8]) {
+      auto store = [&](int h, const uint32_t (&pk)[NCH][8]) __attribute__((always_inline)) {
         const int64_t rq = rowq + h * 256;
         if (rq >= p.n) return;  // warp-uniform
         if (p.debug & kDbgNoStore) return;

@@ -92,3 +92,24 @@ def test_scaled_lift_other_patterns(slsp, z, l):
     p0, s0 = slsp.fused_quant_slide(x, z, l)
     p1, s1 = slsp.fused_quant_slide(x, z, l, absmax=a)
     assert torch.equal(p0, p1) and torch.equal(s0, s1)
+
+
+@pytest.mark.parametrize("n,m", [(1000, 500), (1536, 8192 - 97), (256, 224 * 3 + 5)])
+def test_token_major_epilogue_ragged(slsp, n, m):
+    """Two-subtile tiles with token-major output (the register epilogue's
+    in-smem transpose) at ragged shapes: identical to the [N][M] output
+    transposed, and the |y|max fold exact."""
+    g = torch.Generator(device="cuda").manual_seed(n + m)
+    k = 1024
+    _, pw, s_ch = layer(slsp, n, k, g)
+    x = (torch.rand(m, k, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    pay, s_tok = slsp.fused_quant_slide(x, 6, 8)
+    with slsp.knobs(SLSP_GEMM_MSUB="2", SLSP_GEMM_BN256_MAXM="0"):
+        assert slsp.sparse_gemm_config(pw, m, slsp.OUT_BF16_MN)["subtiles"] == 2
+        y_nm = slsp.sparse_gemm(pw, pay, s_ch=s_ch, s_tok=s_tok, out_mode=slsp.OUT_BF16_NM)
+        y_mn = slsp.sparse_gemm(pw, pay, s_ch=s_ch, s_tok=s_tok, out_mode=slsp.OUT_BF16_MN)
+        amax = torch.empty(m, device="cuda")
+        y_mn2 = slsp.sparse_gemm(pw, pay, s_ch=s_ch, s_tok=s_tok, out_mode=slsp.OUT_BF16_MN, tok_amax=amax)
+    assert torch.equal(y_mn, y_nm.t().contiguous())
+    assert torch.equal(y_mn2, y_mn)
+    assert torch.equal(amax, y_mn.float().abs().amax(dim=1))
