@@ -56,6 +56,9 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--sharded-lift", action="store_true",
+                    help="N>1: each rank holds a K-slice of X and lifts it into every rank's payload over CUDA-IPC "
+                         "peer writes (DESIGN §7) instead of lifting the replicated X")
     return ap.parse_args()
 
 
@@ -175,13 +178,14 @@ def run_b200(args, world, rank, local):
     # replicated on every rank (same seed)
     xgen = torch.Generator(device=device).manual_seed(99)
     xs = [(torch.rand((m, L.k), device=device, generator=xgen) * 2 - 1).to(torch.bfloat16) for L in layers]
-    # N>1: each layer's input arrives K-sharded (the previous layer's output
-    # features are spread over the ranks); the sharded lift lifts
-    # this rank's column slice with the all-reduced |x|max straight into every
-    # rank's payload over NVLink (CUDA IPC peer writes), so each rank lifts
-    # 1/world of X and no all-gather of X or of the payload follows
+    # N>1 (north_star): activations replicated on every rank, each rank lifts
+    # X and runs the GEMM of its N-shard, no collective on the GEMM. With
+    # --sharded-lift each layer's input arrives K-sharded instead (the previous
+    # layer's output features are spread over the ranks) and the sharded lift
+    # lifts this rank's column slice with the all-reduced |x|max
+    # straight into every rank's payload over NVLink (CUDA IPC peer writes)
     sliced = []
-    if world > 1:
+    if world > 1 and args.sharded_lift:
         from paper_2603_05232_b200.sharding import ShardedLift
 
         for i, L in enumerate(layers):
@@ -195,7 +199,7 @@ def run_b200(args, world, rank, local):
     # Each kernel call of the step is captured into a CUDA graph, so the timed
     # region measures device time, not Python launch latency.
     def op_lift(L, i):
-        if world > 1:
+        if world > 1 and args.sharded_lift:
             return lambda: L.sl(sliced[i])
         return lambda: slsp.fused_quant_slide(xs[i], z, l, kp=L.kp, check=False, payload=L.payload,
                                               scales=L.s_tok)
@@ -388,7 +392,8 @@ def run_b200(args, world, rank, local):
                 "X = U(-1,1) bf16, seeded",
         "config": {"workload": f"{args.workload} all linear shapes, {args.pattern} INT8 W8A8, M={m} prefill",
                    "m": m, "pattern": args.pattern, "layers": [f"{n}x{k}" for _, n, k in WORKLOADS[args.workload]],
-                   "step": "per layer: fused_quant_slide(bf16 X) + sparse GEMM, bf16 dequant epilogue" if world == 1
+                   "step": "per layer: fused_quant_slide(bf16 X) + sparse GEMM, bf16 dequant epilogue"
+                   if world == 1 or not args.sharded_lift
                    else "per layer: sharded lift (row_absmax of this rank's K-slice, NCCL all_reduce MAX, "
                         "lift into every rank's payload over NVLink IPC, NCCL barrier) + sparse GEMM on the "
                         "rank's N-shard; dense step: replicated quantize_rows + dense GEMM",

@@ -164,6 +164,49 @@ def cfg5(reps, rows):
                      "speedup": tot_d / tot_s})
 
 
+def cfg5s(reps, rows, nvlink_gbs=900.0):
+    """Config 5 with the K-sharded lift, the per-GPU work of rank 0
+    of G on one GPU: per layer the lift of its K/G column slice with the global
+    |x|max (slsp_fused_quant_slide_scaled_multi, one destination — the local
+    write; the G-1 peer copies are the same kernel's NVLink stores) + the GEMM
+    of its N/G rows on the full payload. NVLink time = the slice's lifted bytes
+    to G-1 peers at `nvlink_gbs` per direction; per-GPU step = sum over layers
+    of max(lift, NVLink) + GEMM (the peer writes overlap the lift kernel)."""
+    from paper_2603_05232_b200.sharding import lifted_col, shard_cols
+
+    m = 8192
+    g = gen()
+    for gpus in (1, 2, 4, 8):
+        tot = tot_lift = tot_gemm = tot_nv = 0.0
+        for name, n, k in QWEN14:
+            per = -(-n // gpus)
+            per = -(-per // 128) * 128
+            w = int8_weights(per, k, 6, 8, g)
+            pw = slsp.pack_compress(w, 6, 8)
+            k0, k1 = shard_cols(k, gpus, 0)
+            x = (torch.rand(m, k1 - k0, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+            amax = slsp.row_absmax(x)
+            payload = torch.zeros((m, pw.kp // 4), dtype=torch.int32, device="cuda")
+            scales = torch.empty(m, device="cuda")
+            s_ch = torch.rand(per, device="cuda", generator=g) * 0.01
+            out = torch.empty((per, m), dtype=torch.bfloat16, device="cuda")
+            t_l = timed(lambda: slsp.fused_quant_slide_multi(x, 6, 8, amax, [payload], pw.kp, lifted_col(k0, 6, 8),
+                                                             scales=scales, check=False), reps)
+            payload.slsp_kind, payload.slsp_pattern = slsp.QUANT_INT8, (6, 8)
+            t_g = timed(lambda: slsp.sparse_gemm(pw, payload, s_ch=s_ch, s_tok=scales, out_mode=slsp.OUT_BF16_NM,
+                                                 out=out), reps)
+            nv_ms = m * (k1 - k0) * 1.5 * (gpus - 1) / (nvlink_gbs * 1e6)
+            tot_lift += t_l
+            tot_gemm += t_g
+            tot_nv += nv_ms
+            tot += max(t_l, nv_ms) + t_g
+            del w, pw, x, payload, out
+        flops = sum(2.0 * m * n * k for _, n, k in QWEN14)
+        rows.append({"cfg": 5, "case": f"qwen2.5-14b 6:8 int8 stack, K-sharded lift, rank 0 of {gpus}",
+                     "step_ms_per_gpu": tot, "lift_ms": tot_lift, "gemm_ms": tot_gemm, "nvlink_ms_projected": tot_nv,
+                     "job_eff_tflops_if_linear": flops / (tot * 1e-3) / 1e12})
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cfg", default="1,3,4,5")
@@ -182,6 +225,7 @@ def main():
         cfg4(a.reps, rows, [int(v) for v in a.ms4.split(",")])
     if 5 in sel:
         cfg5(a.reps, rows)
+        cfg5s(a.reps, rows)
     for r in rows:
         print(json.dumps({k: (round(v, 4) if isinstance(v, float) else v) for k, v in r.items()}), flush=True)
     if a.out:
