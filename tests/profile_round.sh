@@ -23,6 +23,6 @@ timeout 600 $NCU -k regex:pack68b_kernel -s 0 -c 1 -o /tmp/prof_pack python test
 python tests/ncu_summary.py /tmp/prof_sgemm.ncu-rep /tmp/prof_dgemm.ncu-rep /tmp/prof_lift.ncu-rep /tmp/prof_pack.ncu-rep \
    > $out/ncu_full.txt 2>&1
 python tests/ncu_summary.py --launches $out/launches.csv > $out/launches_summary.txt 2>&1
-for f in sgemm dgemm pack; do cp /tmp/prof_$f.ncu-rep $out/ 2>/dev/null; done
+cp /tmp/prof_sgemm.ncu-rep $out/ 2>/dev/null  # (one report: gpurun pulls at most 64 MiB)
 ls -la $out/*.ncu-rep
 echo done
