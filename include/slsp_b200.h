@@ -295,6 +295,23 @@ SLSP_API int slsp_sparse_gemm_config(int dtype, int64_t n, int64_t kp, int64_t m
 SLSP_API int slsp_dense_gemm_config(int dtype, int64_t n, int64_t k, int64_t m, int out_mode, int64_t ws_bytes,
                                     slsp_gemm_config* cfg);
 
+/* BF16 sparse GEMM with the activation lift inside the kernel (decode-shaped
+ * M). x is the UNLIFTED BF16 activation (m x cols, row
+ * stride x_ld elements, even; x 4-byte aligned; cols % l == 0); values/meta
+ * as for slsp_sparse_gemm (slsp_pack_compress + slsp_tile_meta, kp lifted
+ * columns). Lift warps in the GEMM read each window's four source elements
+ * (quantize.hpp:72-89 lift_row) from x and write them straight into the
+ * shared-memory B stage, so no lifted copy of x is ever written. Equals
+ * slsp_sparse_gemm(values, meta, slsp_lift_rows(x, z, l, kp)) bit for bit.
+ * Replaces the lift_row + gemm.hpp:199-233 pair of the reference's BF16 path.
+ * workspace: split-K slices as for slsp_sparse_gemm_ws (NULL: no split). */
+SLSP_API int slsp_sparse_gemm_lift(int dtype, const void* values, const uint8_t* meta, int64_t n, int64_t kp,
+                                   const void* x, int64_t x_ld, int64_t m, int64_t cols, int z, int l,
+                                   const float* s_ch, const float* s_tok, int out_mode, void* out, int64_t ldo,
+                                   void* workspace, int64_t ws_bytes, slsp_stream_t stream);
+SLSP_API int slsp_sparse_gemm_lift_config(int dtype, int64_t n, int64_t kp, int64_t m, int64_t cols, int z, int l,
+                                          int out_mode, int64_t ws_bytes, slsp_gemm_config* out);
+
 /* gemm.hpp:142-197 generic instantiations (T = int32 -> int64 accumulators,
  * T = float -> double) on the CUDA cores, for the drop-in's Matrix<int> /
  * Matrix<float> calls: one thread per output element sums in the reference's

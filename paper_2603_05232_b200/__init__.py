@@ -10,7 +10,7 @@ from ._native import (  # noqa: F401
     PackedWeights, PlanError, SlspError, UnsupportedError, compress, dense_gemm, dense_gemm_config, device_supported,
     fused_quant_slide, fused_quant_slide_multi, gemm_order, ipc_close, ipc_handle, ipc_open, knobs, lib, lift_rows,
     lifted_width, magnitude_prune, pack_compress, pack_matrix, plan_decomposition, quantize_rows, reload_knobs,
-    round_up, row_absmax, sparse_gemm, sparse_gemm_config, sparse_gemm_x, tile_meta,
+    round_up, row_absmax, sparse_gemm, sparse_gemm_config, sparse_gemm_lift, sparse_gemm_x, tile_meta,
 )
 
 from . import container  # noqa: F401,E402

@@ -135,6 +135,10 @@ def lib() -> C.CDLL:
                 "slsp_tiled_meta_bytes": (i64, [i64, i64]),
                 "slsp_reload_knobs": (None, []),
                 "slsp_sparse_gemm_config": (i32, [i32, i64, i64, i64, i32, i64, C.POINTER(GemmConfig)]),
+                "slsp_sparse_gemm_lift": (i32, [i32, vp, vp, i64, i64, vp, i64, i64, i64, i32, i32, vp, vp, i32, vp,
+                                                i64, vp, i64, vp]),
+                "slsp_sparse_gemm_lift_config": (i32, [i32, i64, i64, i64, i64, i32, i32, i32, i64,
+                                                       C.POINTER(GemmConfig)]),
                 "slsp_dense_gemm_config": (i32, [i32, i64, i64, i64, i32, i64, C.POINTER(GemmConfig)]),
             }
             for name, (res, args) in sigs.items():
@@ -629,6 +633,36 @@ def sparse_gemm(w: PackedWeights, act: torch.Tensor, s_ch: torch.Tensor | None =
     _check(lib().slsp_sparse_gemm_ws(w.dtype, _ptr(_raw(w.values)), _ptr(w.tiled()), w.n, w.kp, _ptr(act), m,
                                      _ptr(s_ch), _ptr(s_tok), out_mode, _ptr(o), ldo, _ptr(ws), wsb,
                                      _stream(act.device)), "sparse_gemm")
+    return o
+
+
+def sparse_gemm_lift(w: PackedWeights, x: torch.Tensor, s_ch: torch.Tensor | None = None,
+                     s_tok: torch.Tensor | None = None, out_mode: int = OUT_RAW_NM,
+                     out: torch.Tensor | None = None) -> torch.Tensor:
+    """BF16 sparse GEMM on the UNLIFTED activations x (m x w.k BF16): the
+    lift (quantize.hpp:72-89 lift_row) runs inside the GEMM's lift warps, so
+    no lifted copy of x is written (decode-shaped M). Equals
+    sparse_gemm(w, lift_rows(x, w.z, w.l, w.kp)) bit for bit."""
+    _require_cuda(s_ch, s_tok)
+    if not x.is_cuda:
+        raise ValueError("slsp_b200 operates on CUDA tensors")
+    if w.values.dtype != torch.bfloat16 or x.dtype != torch.bfloat16:
+        raise UnsupportedError("sparse_gemm_lift: BF16 weights and activations")
+    if x.dim() != 2 or x.shape[1] != w.k:
+        raise DimensionMismatchError(f"activation rows must hold k = {w.k} BF16 values")
+    if x.stride(1) != 1:
+        x = x.contiguous()
+    m = x.shape[0]
+    _require_scales(s_ch, "s_ch", w.n, x.device)
+    _require_scales(s_tok, "s_tok", m, x.device)
+    o = _gemm_out(out_mode, w.n, m, False, x.device, out)
+    ldo = o.shape[1]
+    wsb0 = int(lib().slsp_gemm_workspace_bytes(w.n, m))
+    ws, wsb = _workspace(lambda q: lib().slsp_sparse_gemm_lift_config(w.dtype, w.n, w.kp, m, w.k, w.z, w.l, out_mode,
+                                                                      wsb0, q), x.device)
+    _check(lib().slsp_sparse_gemm_lift(w.dtype, _ptr(w.values), _ptr(w.tiled()), w.n, w.kp, _ptr(x), x.stride(0), m,
+                                       w.k, w.z, w.l, _ptr(s_ch), _ptr(s_tok), out_mode, _ptr(o), ldo, _ptr(ws), wsb,
+                                       _stream(x.device)), "sparse_gemm_lift")
     return o
 
 

@@ -39,7 +39,8 @@ constexpr int kNumThreads = 192;
 // emulation: the L2 traffic of a kernel that builds those stages in smem).
 // bit6 (LIFT) skips the C-block build, bit7 (LIFT) skips its proxy fence.
 enum : uint32_t { kDbgNoStore = 1u, kDbgNoLoad = 2u, kDbgSameTile = 4u, kDbgNoMeta = 8u, kDbgNoMma = 16u,
-                  kDbgSkipB3 = 32u, kDbgNoBuild = 64u, kDbgNoFence = 128u, kDbgNoAmaxAtomic = 256u };
+                  kDbgSkipB3 = 32u, kDbgNoBuild = 64u, kDbgNoFence = 128u, kDbgNoAmaxAtomic = 256u,
+                  kDbgNoSts = 512u };
 // L2 cache-policy hints (env SLSP_GEMM_HINTS overrides kDefaultHints).
 enum : uint32_t { kHintBLast = 1u, kHintAFirst = 2u, kHintOutFirst = 4u };
 constexpr uint32_t kDefaultHints = kHintBLast | kHintOutFirst;
@@ -85,9 +86,18 @@ struct Cfg {
   // window 1 (bytes 2-5) of those 64 blocks, which LIFT_WARPS build in shared
   // memory from the two X tiles. The lifted activation never exists in HBM
   // or L2, and a third of the B operand's L2->SM traffic disappears.
-  static constexpr bool LIFT = LIFT_ != 0;
+  static constexpr bool LIFT = LIFT_ == 1;
   static_assert(!LIFT || SPARSE, "in-SM lifting feeds the sparse kernel");
-  static constexpr int LIFT_WARPS = LIFT ? 2 : 0;
+  // GLIFT (LIFT_ == 2, decode-shaped BF16): the lift happens inside the
+  // GEMM — four lift warps build each ring stage's B tile (the lifted
+  // activations of this CTA's tokens) straight from the unlifted BF16 X in
+  // global memory (L2-resident at decode M), so no lift kernel runs at all.
+  static constexpr bool GLIFT = LIFT_ == 2;
+  static_assert(!GLIFT || (SPARSE && KIND == MmaKind::F16 && MSUB == 1), "in-GEMM lift: BF16 one-subtile tiles");
+  static constexpr int GLIFT_GROUPS = 4, GLIFT_GW = 2;  // stage groups x warps per group
+  static constexpr int LIFT_WARPS = LIFT ? 2 : GLIFT ? GLIFT_GROUPS * GLIFT_GW : 0;
+  // lift-warp arrivals per CTA on a stage's full barrier
+  static constexpr int LIFT_ARRIVE = LIFT ? LIFT_WARPS : GLIFT ? GLIFT_GW : 0;
   // double-buffered accumulators where two (and the sparse metadata
   // columns) fit the 512 TMEM columns: one-subtile tiles up to 224 tokens
   // (sparse) / 256 (dense); 256-token sparse tiles drain in between
@@ -221,6 +231,12 @@ struct Params {
   // a NaN |y| (0x7FC0.. > Inf) wins, so the consumer sees the row as
   // non-finite). The next layer's lift then needs no |x|max pass of its own.
   uint32_t* amax;
+  // GLIFT: the unlifted BF16 X (m x k, row stride x_ld elements) and the
+  // pattern's window geometry (l, windows per block, lifted windows per row)
+  const void* x;
+  int64_t x_ld;
+  int lift_l, lift_wc;
+  int64_t lift_windows;
 };
 
 // Fold |bf16| of 2*NW token columns (packed in w, token i = half i&1 of
@@ -564,9 +580,9 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       // LIFT: + one arrival per lift warp of both CTAs ("X present" / "C built")
-      mbar_init(&full[s], 1 + 2 * C::LIFT_WARPS);
+      mbar_init(&full[s], 1 + 2 * C::LIFT_ARRIVE);
       // MMA commit (+ LIFT: each local lift warp is done reading the stage's X tile)
-      mbar_init(&empty[s], C::NPAIR + C::LIFT_WARPS);
+      mbar_init(&empty[s], C::NPAIR + (C::LIFT ? C::LIFT_WARPS : 0));
       mbar_init(&xfull[s], 1);
       mbar_init(&full1[s], 1);
     }
@@ -638,7 +654,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
                 if constexpr (C::SPARSE)
                   tma_prefetch_l2_2d(&tmE, 0, (((a2 + h * 256) >> 7) * p.num_kb + k2) * 8 * C::E_ATOMS);
               }
-              if constexpr (!C::LIFT)
+              if constexpr (!C::LIFT && !C::GLIFT)
 #pragma unroll
                 for (int at = 0; at < C::B_ATOMS; ++at) tma_prefetch_l2_2d(&tmB, k2 * C::K_BYTES_B + at * 128, b2);
             }
@@ -662,7 +678,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
             const bool skip_b = !C::LIFT && (p.debug & kDbgSkipB3) && kb % 3 == 2;
             const bool split = C::SPLIT && p.splitbar;
             const uint32_t tx_all = 2 * (C::STAGE_TX - (skip_e ? C::E_STAGE : 0) -
-                                         ((skip_b || C::LIFT) ? C::B_STAGE : 0));
+                                         ((skip_b || C::LIFT || C::GLIFT) ? C::B_STAGE : 0));
             const uint32_t tx1 = split ? 2 * (C::A_SUB + (skip_e ? 0 : C::E_SUB)) : 0;
             if (leader) {
               mbar_arrive_expect_tx(&full[stage], tx_all - tx1);
@@ -698,7 +714,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
                   tma_load_2d_hint(sB + stage * C::B_STAGE + at * C::B_ATOM, &tmB, smem_u32(&xfull[stage]),
                                    k0 + at * 128, b_row, pol_b);
               }
-            } else {
+            } else if constexpr (!C::GLIFT) {
 #pragma unroll
               for (int at = 0; at < C::B_ATOMS; ++at) {
                 if (skip_b) break;
@@ -881,6 +897,136 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         SLSP_TRACE(it, 2);
         if (p.trace && blockIdx.x == 0) p.trace[it * 16 + 8] = wait_cycles;
         tc_commit_mc(&tfull[acc], pair_epi);
+      }
+    }
+  } else if (C::GLIFT && warp >= 2 + C::EPI_WARPS) {
+    // ------------------------------------------- in-GEMM lift warps ----
+    // GLIFT_GROUPS groups of GLIFT_GW warps; group g takes every
+    // GLIFT_GROUPS-th stage of the producer's sequence, so that many stages'
+    // L2 reads are in flight at once. GLIFT_GROUPS <= STAGES keeps every
+    // empty-barrier wait within one phase of the barrier: the group's
+    // previous stage q - G needed stage q - G - STAGES consumed, so the slot's
+    // occupant before q - STAGES is gone (parity waits cannot tell phases two
+    // apart). Per stage: wait for the ring slot,
+    // build the stage's B tile for this CTA's tokens — lifted BF16 element e
+    // (window j = e/4: source elements l*(j/wc) + 2*(j%wc) + 0..3,
+    // quantize.hpp:72-89 lift_row; windows past the real ones are the zero
+    // padding up to kp) — as 16-byte chunks of two windows in the 128B
+    // swizzle the UMMA descriptor expects, fence the generic-proxy writes to
+    // the async proxy, and arrive on the leader's full barrier. Rows of
+    // tokens past m are left as they are: their accumulator columns are
+    // never stored.
+    if constexpr (C::GLIFT) {
+      const uint32_t lw = warp - 2 - C::EPI_WARPS;
+      const uint32_t grp = lw / C::GLIFT_GW;
+      const uint32_t gt = (lw % C::GLIFT_GW) * 32 + lane_id();  // thread within the group
+      const uint32_t full_lead = mapa_shared(smem_u32(&full[0]), lead);
+      constexpr int CHUNKS = C::B_ATOMS * 8;  // 16-byte chunks per token row per stage
+      constexpr int ITER = C::B_ROWS * CHUNKS / (C::GLIFT_GW * 32);
+      static_assert(ITER * C::GLIFT_GW * 32 == C::B_ROWS * CHUNKS, "lift group covers the B tile exactly");
+      static_assert(C::GLIFT_GROUPS <= C::STAGES, "lift groups run at most one ring lap apart");
+      const uint16_t* X = static_cast<const uint16_t*>(p.x);
+      const bool no_ldg = p.debug & kDbgNoBuild, no_sts = p.debug & kDbgNoSts;  // perf probing
+      // 6:8 path geometry: 8 lanes per token row, RPI rows per iteration
+      constexpr int RPI = 4 * C::GLIFT_GW;
+      constexpr int IT = C::B_ROWS / RPI;
+      static_assert(IT * RPI == C::B_ROWS, "6:8 path: whole rows per iteration");
+      const int tl = static_cast<int>(lane_id() & 7);  // triple lane
+      const int rsub = static_cast<int>(gt >> 3);      // row within an iteration
+      const int wrow0 = static_cast<int>((gt & ~31u) >> 3);  // this warp's first row within an iteration
+      const int groups = static_cast<int>(p.lift_windows / 3);
+      int stage = 0, cnt = 0;
+      uint32_t phase = 0;
+      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
+        int mt_, ns, kb0, kb1;
+        tile_coords(tile, p, p.m_tiles, n_super, mt_, ns, kb0, kb1);
+        const int64_t t_first = static_cast<int64_t>(ns) * C::BN + rank * C::B_ROWS;
+        const int rows = static_cast<int>(imin64(C::B_ROWS, p.m - t_first));  // valid token rows (may be <= 0)
+        const uint16_t* rp[IT];  // this thread's token rows (6:8 path)
+#pragma unroll
+        for (int i = 0; i < IT; ++i) rp[i] = X + (t_first + i * RPI + rsub) * p.x_ld;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          if (cnt == static_cast<int>(grp)) {
+          const uint32_t dst = smem_u32(sB + stage * C::B_STAGE);
+          if (p.lift_l == 8) {
+            // 6:8 on 16-byte aligned rows, by "triples": chunks 3t..3t+2
+            // (windows 6t..6t+5) are exactly source blocks 2t and 2t+1:
+            //   chunk 3t   = x[0..3]  x[2..5]   of block 2t
+            //   chunk 3t+1 = x[4..7] of 2t,  x[0..3] of 2t+1
+            //   chunk 3t+2 = x[2..5]  x[4..7]   of block 2t+1
+            // so lane tl of a row loads two blocks (2 x LDG.128, 32
+            // contiguous bytes) and stores the triple's chunks that fall in
+            // this stage (16 chunks: <= 7 triples) — fixed selects, no
+            // shuffles. Blocks past the row's last are zero (padding windows).
+            const int c0 = kb * CHUNKS;
+            const int t = c0 / 3 + tl;
+            const bool act = 3 * t < c0 + CHUNKS;
+            const bool va = act && 2 * t < groups && !no_ldg, vb = act && 2 * t + 1 < groups && !no_ldg;
+            uint4 va4[IT], vb4[IT];
+#pragma unroll
+            for (int i = 0; i < IT; ++i) {
+              const bool live = i * RPI + rsub < rows;
+              const uint4* src = reinterpret_cast<const uint4*>(rp[i] + 16 * t);
+              va4[i] = (live && va) ? __ldg(src) : make_uint4(0u, 0u, 0u, 0u);
+              vb4[i] = (live && vb) ? __ldg(src + 1) : make_uint4(0u, 0u, 0u, 0u);
+            }
+            mbar_wait(&empty[stage], phase ^ 1);
+            const int cc0 = 3 * t - c0;  // stage-local chunk of the triple's first chunk (may be < 0)
+#pragma unroll
+            for (int i = 0; i < IT; ++i) {
+              if (i * RPI + wrow0 >= rows || no_sts) break;  // warp-uniform: no valid row left for this warp
+              const int r = i * RPI + rsub;
+              const uint32_t rb = dst + r * 128;
+              const uint32_t sw = static_cast<uint32_t>(r & 7);
+              const uint4 A = va4[i], B = vb4[i];
+              if (act && cc0 >= 0)
+                st_shared_v4(rb + (cc0 >> 3) * C::B_ATOM + (((cc0 & 7) ^ sw) << 4), A.x, A.y, A.y, A.z);
+              if (act && cc0 + 1 >= 0 && cc0 + 1 < CHUNKS)
+                st_shared_v4(rb + ((cc0 + 1) >> 3) * C::B_ATOM + ((((cc0 + 1) & 7) ^ sw) << 4), A.z, A.w, B.x, B.y);
+              if (act && cc0 + 2 >= 0 && cc0 + 2 < CHUNKS)
+                st_shared_v4(rb + ((cc0 + 2) >> 3) * C::B_ATOM + ((((cc0 + 2) & 7) ^ sw) << 4), B.y, B.z, B.z, B.w);
+            }
+          } else {
+            const int lift_l = p.lift_l < 0 ? -p.lift_l : p.lift_l;  // -8: 6:8 on unaligned rows
+            uint32_t w[ITER][4];
+#pragma unroll
+            for (int i = 0; i < ITER; ++i) {
+              const int u = static_cast<int>(gt) + i * C::GLIFT_GW * 32;
+              const int r = u / CHUNKS, cc = u % CHUNKS;
+              const int64_t j0 = (static_cast<int64_t>(kb) * (C::B_ATOMS * 64) + cc * 8) >> 2;  // first window
+              const uint16_t* xr = X + (t_first + r) * p.x_ld;
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {  // two windows per chunk
+                const int64_t j = j0 + h;
+                w[i][2 * h] = 0u;
+                w[i][2 * h + 1] = 0u;
+                if (r < rows && j < p.lift_windows && !no_ldg) {
+                  const int64_t g = j / p.lift_wc;
+                  const uint32_t* src = reinterpret_cast<const uint32_t*>(xr + g * lift_l + 2 * (j - g * p.lift_wc));
+                  w[i][2 * h] = __ldg(src);
+                  w[i][2 * h + 1] = __ldg(src + 1);
+                }
+              }
+            }
+            mbar_wait(&empty[stage], phase ^ 1);
+#pragma unroll
+            for (int i = 0; i < ITER; ++i) {
+              const int u = static_cast<int>(gt) + i * C::GLIFT_GW * 32;
+              const int r = u / CHUNKS, cc = u % CHUNKS;
+              st_shared_v4(dst + (cc >> 3) * C::B_ATOM + r * 128 + (((cc & 7) ^ (r & 7)) << 4), w[i][0], w[i][1],
+                           w[i][2], w[i][3]);
+            }
+          }
+          if (!(p.debug & kDbgNoFence)) fence_async_smem();  // generic-proxy writes -> visible to the tensor core
+          __syncwarp();
+          if (lane_id() == 0) mbar_arrive_cluster(full_lead + 8u * stage);
+          }
+          if (++cnt == C::GLIFT_GROUPS) cnt = 0;
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
       }
     }
   } else if (C::LIFT && warp >= 2 + C::EPI_WARPS) {
@@ -1676,6 +1822,67 @@ int sparse_entry(int dtype, const void* values, const uint8_t* meta, int64_t n, 
   return run_out<true, MmaKind::F8, kSparseBN, L>(out_mode, ta, tb, te, to, p, s, msub, kh, q, npair);
 }
 
+// slsp_sparse_gemm_lift: the BF16 sparse GEMM on the UNLIFTED activations
+// (x: m x cols BF16, row stride x_ld elements); the kernel's lift warps build
+// every B stage from x (Cfg::GLIFT). Decode tiles (64 tokens, one subtile) at
+// every m; split-K as for sparse_gemm. Equals
+// sparse_gemm(values, lift_rows(x, z, l, kp)) bit for bit.
+int glift_entry(const void* values, const uint8_t* meta, int64_t n, int64_t kp, const void* x, int64_t x_ld, int64_t m,
+                int64_t cols, int z, int l, const float* s_ch, const float* s_tok, int out_mode, void* out,
+                int64_t ldo, void* ws, int64_t ws_bytes, slsp_stream_t stream, slsp_gemm_config* q = nullptr) {
+  using namespace slsp_host;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (n < 0 || m < 0 || kp <= 0 || cols < 0) return SLSP_ERR_INVALID;
+  int wc = 0;
+  int st = plan(z, l, &wc);
+  if (st) return st;
+  if (kp % 256 != 0 || cols % l != 0) return SLSP_ERR_DIMENSION;  // quantize.hpp:78-81
+  const int64_t windows = cols / l * wc;
+  if (kp < windows * 4) return SLSP_ERR_DIMENSION;
+  if (n > (int64_t{1} << 31) - 256 || m > (int64_t{1} << 31) - 256) return SLSP_ERR_UNSUPPORTED;
+  if (out_mode != SLSP_OUT_RAW_NM && out_mode != SLSP_OUT_BF16_NM && out_mode != SLSP_OUT_BF16_MN)
+    return SLSP_ERR_INVALID;
+  if (!q && (st = check_out(out_mode, s_ch, s_tok, out, ldo, n, m))) return st;
+  if (!q && m > 0 && (!x || x_ld < cols || (x_ld & 1) || (reinterpret_cast<uintptr_t>(x) & 3)))
+    return SLSP_ERR_INVALID;  // window loads are 4-byte aligned pairs of BF16
+  if ((st = require_sm100())) return st;
+  if (!q && (n == 0 || m == 0)) return SLSP_OK;
+  CUtensorMap ta{}, tb{}, te{}, to{};
+  Params p{};
+  if (ws && ws_bytes >= 2 * n * m * 4) {
+    p.ws = ws;
+    p.ws_cap = ws_bytes;
+  }
+  if (!q) {
+    if ((st = make_map_2d(&ta, values, kp, n, 128, 128))) return st;  // kp/2 BF16 values per row
+    if ((st = make_map_meta(&te, meta, n, kp, 8))) return st;
+    if ((st = make_map_out(&to, out, out_mode, n, m, ldo, epi_cols(1, kDecodeBN, out_mode), &p.tma_store))) return st;
+    select_epilogue(p, out_mode, 1, out, ldo, s_tok);
+    tb = ta;  // unused: no B loads
+  }
+  p.n = n;
+  p.m = m;
+  p.num_kb = static_cast<int>(kp / 128);
+  p.s_ch = s_ch;
+  p.s_tok = s_tok;
+  p.out = out;
+  p.ldo = ldo;
+  p.debug = debug_flags();
+  p.trace = reinterpret_cast<unsigned long long*>(env_ptr("SLSP_GEMM_TRACE"));
+  p.hints = env_knob("SLSP_GEMM_HINTS", kDefaultHints);
+  p.group = static_cast<int>(env_knob("SLSP_GEMM_GROUP", kRasterGroup));
+  p.splitbar = static_cast<int>(env_knob("SLSP_GEMM_SPLITBAR", 1));
+  p.tail0 = static_cast<int>(env_knob("SLSP_GEMM_TAIL0", kTail0));
+  p.x = x;
+  p.x_ld = x_ld;
+  p.lift_l = l;
+  // the 6:8 path loads whole 16-byte source blocks: rows 16-byte aligned
+  if (l == 8 && ((reinterpret_cast<uintptr_t>(x) & 15) || (x_ld & 7))) p.lift_l = -8;
+  p.lift_wc = wc;
+  p.lift_windows = windows;
+  return run_out_cl<true, MmaKind::F16, kDecodeBN, 1, 2, 0>(out_mode, ta, tb, te, to, p, s, q);
+}
+
 int dense_entry(int dtype, const void* w, int64_t n, int64_t k, const void* act, int64_t m, const float* s_ch,
                 const float* s_tok, int out_mode, void* out, int64_t ldo, void* workspace, int64_t ws_bytes,
                 slsp_stream_t stream, slsp_gemm_config* q = nullptr) {
@@ -1800,6 +2007,26 @@ int slsp_dense_gemm_ws(int dtype, const void* w, int64_t n, int64_t k, const voi
                        const float* s_tok, int out_mode, void* out, int64_t ldo, void* workspace, int64_t ws_bytes,
                        slsp_stream_t stream) {
   return dense_entry(dtype, w, n, k, act, m, s_ch, s_tok, out_mode, out, ldo, workspace, ws_bytes, stream);
+}
+
+int slsp_sparse_gemm_lift(int dtype, const void* values, const uint8_t* meta, int64_t n, int64_t kp, const void* x,
+                          int64_t x_ld, int64_t m, int64_t cols, int z, int l, const float* s_ch, const float* s_tok,
+                          int out_mode, void* out, int64_t ldo, void* workspace, int64_t ws_bytes,
+                          slsp_stream_t stream) {
+  if (dtype != SLSP_DT_BF16) return SLSP_ERR_UNSUPPORTED;
+  return glift_entry(values, meta, n, kp, x, x_ld, m, cols, z, l, s_ch, s_tok, out_mode, out, ldo, workspace, ws_bytes,
+                     stream);
+}
+
+int slsp_sparse_gemm_lift_config(int dtype, int64_t n, int64_t kp, int64_t m, int64_t cols, int z, int l,
+                                 int out_mode, int64_t ws_bytes, slsp_gemm_config* out) {
+  if (!out) return SLSP_ERR_INVALID;
+  if (dtype != SLSP_DT_BF16) return SLSP_ERR_UNSUPPORTED;
+  *out = slsp_gemm_config{};
+  // a non-null dummy so the config reflects a call that can split
+  void* ws = ws_bytes > 0 ? reinterpret_cast<void*>(uintptr_t{256}) : nullptr;
+  return glift_entry(nullptr, nullptr, n, kp, nullptr, cols, m, cols, z, l, nullptr, nullptr, out_mode, nullptr, 0, ws,
+                     ws_bytes, nullptr, out);
 }
 
 }  // extern "C"

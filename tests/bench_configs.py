@@ -128,12 +128,18 @@ def cfg4(reps, rows, ms):
             t_s = timed(lambda: slsp.sparse_gemm(pw, lifted, out=ys), reps)
             yd = slsp.dense_gemm(w, x)
             t_d = timed(lambda: slsp.dense_gemm(w, x, out=yd), reps)
+            # the lift inside the GEMM (sparse_gemm_lift): the whole sparse step in one kernel
+            yg = slsp.sparse_gemm_lift(pw, x)
+            assert torch.equal(yg, ys), "sparse_gemm_lift != sparse_gemm(lift_rows)"
+            t_g = timed(lambda: slsp.sparse_gemm_lift(pw, x, out=yg), reps)
             sb = n * pw.kp // 2 * 2 + n * pw.kp // 8 + m * pw.kp * 2 + n * m * 4
+            gb = n * pw.kp // 2 * 2 + n * pw.kp // 8 + m * k * 2 + n * m * 4
             db = n * k * 2 + m * k * 2 + n * m * 4
             rows.append({"cfg": 4, "case": f"6:8 bf16 {name} M={m}", "lift_us": t_lift * 1e3, "sparse_us": t_s * 1e3,
                          "sparse_gbs": sb / t_s / 1e6, "sparse_hbm_frac": sb / t_s / 1e6 / HBM,
+                         "glift_us": t_g * 1e3, "glift_hbm_frac": gb / t_g / 1e6 / HBM,
                          "dense_us": t_d * 1e3, "dense_gbs": db / t_d / 1e6, "speedup": t_d / t_s,
-                         "bound": db / sb})
+                         "step_speedup_glift": t_d / t_g, "bound": db / sb})
 
 
 def cfg5(reps, rows):

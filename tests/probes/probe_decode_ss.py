@@ -93,7 +93,10 @@ def main():
                     sp_g = [(lambda j: lambda: slsp.sparse_gemm(pws[j], lifted, out=ys))(i % copies)
                             for i in range(a.calls)]
                     de = [(lambda j: lambda: slsp.dense_gemm(ws[j], x, out=ys))(i % copies) for i in range(a.calls)]
+                    gl = [(lambda j: lambda: slsp.sparse_gemm_lift(pws[j], x, out=ys))(i % copies)
+                          for i in range(a.calls)]
                 else:
+                    gl = None
                     pay, st = slsp.fused_quant_slide(x, 6, 8, kp=kp)
                     q, qs = slsp.quantize_rows(x)
                     ys = torch.empty((n, m), dtype=torch.int32, device="cuda")
@@ -108,11 +111,14 @@ def main():
                 t_sp = run_graph(sp) / a.calls
                 t_g = run_graph(sp_g) / a.calls
                 t_de = run_graph(de) / a.calls
+                t_gl = run_graph(gl) / a.calls if gl else None
                 sb = n * kp // 2 * (2 if bf16 else 1) + n * kp // 8
                 db = n * k * (2 if bf16 else 1)
                 print(json.dumps({"case": f"{case} {n}x{k} M={m}", "knobs": kv, "sparse_step_us": round(t_sp, 2),
                                   "sparse_gemm_us": round(t_g, 2), "dense_step_us": round(t_de, 2),
                                   "step_speedup": round(t_de / t_sp, 3),
+                                  "glift_step_us": round(t_gl, 2) if t_gl else None,
+                                  "glift_speedup": round(t_de / t_gl, 3) if t_gl else None,
                                   "gemm_weight_gbs": round(sb / t_g / 1e3, 1), "dense_weight_gbs": round(db / t_de / 1e3, 1),
                                   "cfg": f"bn{cfg['tokens_per_tile']} ks{cfg['ksplit']} cl{cfg['clusters']}"}),
                       flush=True)

@@ -1,7 +1,8 @@
 """Minimal ncu targets (GPU box; perf probing): runs one op 4 times after L2
 flushes. Modes: cfg1_sparse / cfg1_dense (6:8 INT8 4096x4096, M=128),
 dec_sparse / dec_dense (Llama-3.1-8B qkv 6144x4096 BF16, M=1), lift_m1 /
-lift_m8192 (fused_quant_slide of a 3584-wide BF16 X), chain_amax (sparse GEMM
+lift_m8192 (fused_quant_slide of a 3584-wide BF16 X), glift_mM / gsparse_mM
+(gate_up 28672x4096 BF16: sparse_gemm_lift vs sparse_gemm on lifted rows), chain_amax (sparse GEMM
 o_proj 3584x3584 M=8192 MN with the token |y|max fold)."""
 import sys
 from pathlib import Path
@@ -27,6 +28,13 @@ elif mode.startswith("dec"):
     pw = slsp.pack_compress(w, 6, 8)
     lifted = slsp.lift_rows(x, 6, 8, kp=pw.kp)
     fn = (lambda: slsp.sparse_gemm(pw, lifted)) if mode == "dec_sparse" else (lambda: slsp.dense_gemm(w, x))
+elif mode.startswith("glift") or mode.startswith("gsparse"):
+    m = int(mode.split("_m")[1])  # Llama-3.1-8B gate_up BF16: in-GEMM lift vs lifted operand
+    w = slsp.magnitude_prune((torch.rand(28672, 4096, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16), 6, 8)
+    x = (torch.rand(m, 4096, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    pw = slsp.pack_compress(w, 6, 8)
+    lifted = slsp.lift_rows(x, 6, 8, kp=pw.kp)
+    fn = (lambda: slsp.sparse_gemm_lift(pw, x)) if mode.startswith("glift") else (lambda: slsp.sparse_gemm(pw, lifted))
 elif mode.startswith("lift"):
     m = int(mode.split("_m")[1])
     if mode.startswith("liftg"):  # gaussian rows with per-row scales (absmax not a power of two)
