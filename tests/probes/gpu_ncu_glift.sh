@@ -8,7 +8,7 @@ done
 python tests/ncu_summary.py /tmp/ncu/g*.ncu-rep > gpurun_out/glift_ncu.txt 2>&1
 for m in glift_m64 gsparse_m64; do
   ncu -i /tmp/ncu/$m.ncu-rep --page raw --csv > /tmp/ncu/$m.raw.csv 2>/dev/null
-  ncu -i /tmp/ncu/$m.ncu-rep --page source --csv --print-source sass > gpurun_out/${m}_source.csv 2>/dev/null
+  true
 done
-cp /tmp/ncu/glift_m64.ncu-rep gpurun_out/
+python tests/ncu_summary.py --grep "inst_executed.sum$|smsp__average_warp|dram__bytes|l1tex__m_xbar2l1tex_read_bytes.sum$|gpu__time_duration" /tmp/ncu/g*.ncu-rep > gpurun_out/glift_ncu_extra.txt 2>&1
 tail -n 2 /tmp/ncu/*.log; ls -la gpurun_out | tail
