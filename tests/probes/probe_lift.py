@@ -42,7 +42,7 @@ for k in [int(v) for v in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["35
     print(f"K={k:6d} calibration: torch copy bf16 {t_c * 1e3:7.1f} us {2 * x.numel() * 2 / t_c / 1e6:7.0f} GB/s",
           flush=True)
     ref = {}
-    for path in ("2", "1"):  # 2: warp path, 1: default (row kernel)
+    for path in (sys.argv[2].split(",") if len(sys.argv) > 2 else ("0", "1")):  # 0 warp, 1 row, 2 row (1024-thread), 3 persistent row
         os.environ["SLSP_LIFT_ROW"] = path
         slsp.reload_knobs()
         t_l = burst(lambda: slsp.fused_quant_slide(x, 6, 8, check=False, payload=pay, scales=sc))
