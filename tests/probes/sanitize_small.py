@@ -4,7 +4,7 @@ Covers: packers (6:8 LUT byte path, generic patterns, bf16), magnitude_prune,
 lift (row-resident, warp, generic, scaled, multi-destination), quantize_rows,
 row_absmax, sparse GEMM configs (int8 two-subtile / one-subtile / 256-token /
 decode split-K, FP8, BF16, both output layouts, amax fold, in-SM lifting),
-dense GEMM (int8, FP8, BF16, decode split-K). Prints one line per step."""
+dense GEMM (int8, FP8, BF16, decode split-K), the in-GEMM BF16 lift. Prints one line per step."""
 import os
 import sys
 from pathlib import Path
@@ -70,6 +70,10 @@ def main():
         lifted = slsp.lift_rows(x, 6, 8, kp=pb.kp)
         step(f"sparse bf16 {tag}", lambda: slsp.sparse_gemm(pb, lifted))
         step(f"dense bf16 {tag}", lambda: slsp.dense_gemm(wb, x))
+        step(f"sparse bf16 in-GEMM lift {tag}", lambda: slsp.sparse_gemm_lift(pb, x, s_ch=s_ch, s_tok=st,
+                                                                            out_mode=slsp.OUT_BF16_NM))
+        xs = torch.zeros((m, k + 2), dtype=torch.bfloat16, device="cuda")[:, :k]  # 4-byte path
+        step(f"sparse bf16 in-GEMM lift strided {tag}", lambda: slsp.sparse_gemm_lift(pb, xs))
         if m >= 64:
             xq, _ = slsp.quantize_rows(x, kpad=slsp.round_up(k, 512))
             step(f"sparse in-SM lift {tag}", lambda: slsp.sparse_gemm_x(p8, xq))
