@@ -290,6 +290,35 @@ def run_b200(args, world, rank, local):
         return acc[0::2], acc[1::2]
 
     sp_lift, sp_gemm = per_op(sparse_op_graphs)
+
+    # The same kernels live inside the step: the step graph re-captured with
+    # timing events between its launches (cudaEventRecordExternal nodes),
+    # replayed after an L2 flush like a timed step; per-kernel durations are
+    # averaged over the replays (the roofline's denominator, below).
+    def in_step(fns, reps=max(3, min(args.steps, 10))):
+        evs = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(len(fns) + 1)]
+        try:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                for j, f in enumerate(fns):
+                    evs[j].record()
+                    f()
+                evs[-1].record()
+        except Exception as e:  # noqa: BLE001
+            print(f"[bench] in-step event capture failed ({e}); per-kernel times from isolated launches",
+                  file=sys.stderr)
+            return None
+        acc = [0.0] * len(fns)
+        for _ in range(reps):
+            flush.zero_()
+            g.replay()
+            torch.cuda.synchronize()
+            for j in range(len(fns)):
+                acc[j] += evs[j].elapsed_time(evs[j + 1]) / reps
+        return acc
+
+    sp_in_step = in_step(sparse_ops)
+    de_in_step = in_step(dense_ops) if dense_ops else None
     de_lift, de_gemm = per_op(dense_op_graphs) if dense_op_graphs else (None, None)
     pack = None if args.no_dense else time_pack(slsp, torch, layers, z, l, timed, per_op, stream)
 
@@ -344,25 +373,46 @@ def run_b200(args, world, rank, local):
                                  "128-row blocks), timed alone after the GEMM step"}
 
     # ---- roofline of the dominant kernel (the sparse GEMM) ----
+    # achieved: executed ops / the GEMM launches' durations measured inside
+    # the timed step (events captured in the step graph); the step is a long
+    # back-to-back run, so the peak is the SUSTAINED measured bf16 figure
+    # (MEASURED_PEAKS.json; the B200 runs GEMM-class work at its power cap,
+    # DESIGN §6.0). The isolated-launch figure against the burst peak is
+    # kept beside it.
     peaks = json.loads(PEAKS_FILE.read_text()) if PEAKS_FILE.exists() else {}
     bf16_peak = peaks.get("bf16_tflops", 1590.0)
+    bf16_sus = peaks.get("bf16_tflops_sustained")
     peak_basis = "measured" if "bf16_tflops" in peaks else "fallback"
     sparse_peak = 2 * 2 * bf16_peak  # int8 dense = 2x bf16 (datasheet ratio); 2:4 sparse pipe = 2x dense
     exec_flops = sum(2.0 * m * L.n * L.kp for L in layers)  # dense-equivalent ops run on the sparse pipe
     gemm_ms = sum(sp_gemm)
-    achieved = exec_flops / (gemm_ms * 1e-3) / 1e12
+    achieved_alone = exec_flops / (gemm_ms * 1e-3) / 1e12
+    gemm_ms_step = sum(sp_in_step[1::2]) if sp_in_step else None
     traffic = None
     if TRAFFIC_FILE.exists():
         tr = json.loads(TRAFFIC_FILE.read_text())
         traffic = tr.get("sparse_gemm_bytes_per_launch")
-    roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": round(sparse_peak, 1),
-                "unit": "TFLOP/s", "frac": round(achieved / sparse_peak, 4), "traffic": traffic,
+    if gemm_ms_step and bf16_sus:
+        achieved = exec_flops / (gemm_ms_step * 1e-3) / 1e12
+        peak = 2 * 2 * bf16_sus
+        basis = (f"measured sustained bf16 {bf16_sus} TF x2 (int8/bf16 datasheet ratio) x2 (2:4 sparse pipe); "
+                 "GEMM launches timed inside the step")
+    else:
+        achieved, peak = achieved_alone, sparse_peak
+        basis = (f"{peak_basis} bf16 {bf16_peak} TF x2 (int8/bf16 datasheet ratio) x2 (2:4 sparse pipe); "
+                 "GEMM launches timed alone")
+    roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": round(peak, 1),
+                "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                 "kernel": "gemm_kernel<sparse,i8> (tcgen05.mma.sp cta_group::2)",
-                "peak_basis": f"{peak_basis} bf16 {bf16_peak} TF x2 (int8/bf16 datasheet ratio) x2 (2:4 sparse pipe)",
+                "peak_basis": basis,
+                "alone_vs_burst": {"achieved": round(achieved_alone, 1), "peak": round(sparse_peak, 1),
+                                   "frac": round(achieved_alone / sparse_peak, 4),
+                                   "basis": f"each GEMM launched alone after an L2 flush vs the burst "
+                                            f"{peak_basis} bf16 {bf16_peak} TF x4"},
                 "frac_of_datasheet_9000": round(achieved / 9000.0, 4),
                 "effective_tflops_gemm_only": round(sum(L.flops for L in layers) / (gemm_ms * 1e-3) / 1e12, 1)}
     lift_bytes = sum(m * (2 * L.k + L.kp + 4) for L in layers)
-    lift_ms = sum(sp_lift)
+    lift_ms = sum(sp_in_step[0::2]) if sp_in_step else sum(sp_lift)
     lift_roofline = {"bound": "hbm", "achieved": round(lift_bytes / (lift_ms * 1e-3) / 1e9, 1),
                      "peak": peaks.get("hbm_gbs", 6650.0), "unit": "GB/s",
                      "frac": round(lift_bytes / (lift_ms * 1e-3) / 1e9 / peaks.get("hbm_gbs", 6650.0), 4)}
@@ -378,6 +428,12 @@ def run_b200(args, world, rank, local):
         row = {"name": L.name, "n": L.n_total, "n_shard": L.n, "k": L.k, "kp": L.kp,
                "lift_ms": round(sp_lift[i], 4), "sparse_gemm_ms": round(sp_gemm[i], 4),
                "sparse_gemm_eff_tflops": round(L.flops / (sp_gemm[i] * 1e-3) / 1e12, 1)}
+        if sp_in_step:
+            row.update({"lift_ms_in_step": round(sp_in_step[2 * i], 4),
+                        "sparse_gemm_ms_in_step": round(sp_in_step[2 * i + 1], 4)})
+        if de_in_step:
+            row.update({"quant_ms_in_step": round(de_in_step[2 * i], 4),
+                        "dense_gemm_ms_in_step": round(de_in_step[2 * i + 1], 4)})
         if de_gemm:
             row.update({"quant_ms": round(de_lift[i], 4), "dense_gemm_ms": round(de_gemm[i], 4),
                         "dense_gemm_tflops": round(L.flops / (de_gemm[i] * 1e-3) / 1e12, 1),
@@ -401,6 +457,8 @@ def run_b200(args, world, rank, local):
                    "l2": "flushed between timed steps (512 MiB write, outside events)"},
         "speedup_vs_dense": round(de_ms_max / sp_ms_max, 4) if de_ms_max else None,
         "gemm_speedup_vs_dense": round(sum(de_gemm) / sum(sp_gemm), 4) if de_gemm else None,
+        "gemm_speedup_vs_dense_in_step": (round(sum(de_in_step[1::2]) / sum(sp_in_step[1::2]), 4)
+                                          if sp_in_step and de_in_step else None),
         "speedup_bound": round(2 * sum(L.k for L in layers) / sum(L.kp for L in layers), 4),
         "dense": {"value": round(dense_value, 2) if dense_value else None,
                   "ms_per_step": round(de_ms_max, 4) if de_ms_max else None,
