@@ -50,7 +50,7 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="qwen2.5-7b")
-    ap.add_argument("--m", type=int, default=8192)
+    ap.add_argument("--m", "--tokens", dest="m", type=int, default=8192)
     ap.add_argument("--pattern", default="6:8")
     ap.add_argument("--out-mode", choices=["nm", "mn"], default="nm")
     ap.add_argument("--no-e2e", action="store_true")
@@ -62,10 +62,15 @@ def parse_args():
     return ap.parse_args()
 
 
+# Test hook (tests/test_gpu_bench_multirank.py): every rank on cuda:0 over
+# gloo, so the N>1 code path runs on a one-GPU box (timings meaningless).
+SHARE_GPU = os.environ.get("SLSP_BENCH_SHARE_GPU") == "1"
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = 0 if SHARE_GPU else int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
 
 
@@ -163,7 +168,10 @@ def run_b200(args, world, rank, local):
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=device)
+        if SHARE_GPU:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=device)
     z, l = (int(v) for v in args.pattern.split(":"))
     m = args.m
     gen = torch.Generator(device=device).manual_seed(1234 + rank)
@@ -474,6 +482,18 @@ def run_b200(args, world, rank, local):
         sparse_graph.replay()
         torch.cuda.synchronize()
         result["cpu_baseline"], result["parity"] = cpu_baseline(slsp, torch, layers, xs, outs, out_mode, z, l)
+    elif world > 1:
+        # every rank checks the sampled rows of its own shard; counts summed over ranks
+        sparse_graph.replay()
+        torch.cuda.synchronize()
+        threads = max(1, (os.cpu_count() or 1) // world)
+        _, kind, _, _, mism, checked, _ = sampled_reference(slsp, torch, layers, xs, outs, out_mode, z, l, threads)
+        cnt = torch.tensor([float(mism), float(checked)], dtype=torch.float64, device=device)
+        torch.distributed.all_reduce(cnt)
+        result["parity"] = {"bit_exact": int(cnt[0].item()) == 0, "mismatches": int(cnt[0].item()),
+                            "outputs_checked": int(cnt[1].item()),
+                            "what": "every rank: BF16 outputs of its N-shard on sampled (row, token) blocks vs the "
+                                    f"CPU {kind} + the a18 dequant restatement; counts summed over ranks"}
     if rank == 0:
         print(json.dumps(result), flush=True)
     if world > 1:
@@ -609,25 +629,26 @@ def extrapolate(t_lift, t_gemm, n, m, rows, toks):
     return t_lift * m / toks + t_gemm * (n * m) / (rows * toks)
 
 
-def cpu_baseline(slsp, torch, layers, xs, outs, out_mode, z, l):
-    """The GPU arm's cpu_baseline leg: the sampled + extrapolated reference
-    step (rank 0, N = 1), the full o_proj timed once, and — since the sample
-    computes exact reference outputs — the parity check of the GPU outputs of
-    the timed step on the sampled (row, token) blocks."""
+def sampled_reference(slsp, torch, layers, xs, outs, out_mode, z, l, threads):
+    """The CPU reference (oracle/_ref, else the port) on every layer's sampled
+    weight rows x all tokens, timed, and its BF16 outputs compared with the
+    GPU outputs `outs` of those (row, token) blocks. With N > 1 each rank
+    samples the rows of its own N-shard."""
     import numpy as np
 
     sys.path.insert(0, str(ROOT / "tests"))
-    from oracle_lib import DT_BF16, DT_I8, KIND_INT8, orc, ref
+    from oracle_lib import DT_I8, orc, ref
 
     R = ref()
     kind = "reference"
     if R is None:
         R, kind = orc(), "port"
     O = orc()  # the a18 dequant restatement (the reference stops at int32)
-    threads = os.cpu_count() or 1
     t_total, mism, checked, t_sample = 0.0, 0, 0, 0.0
     per_layer = []
     for i, L in enumerate(layers):
+        if L.n == 0:
+            continue
         rows, toks = sample_rows(L.n), sample_tokens(L.m)
         ri, ti = torch.tensor(rows, device=xs[i].device), torch.tensor(toks, device=xs[i].device)
         vals, codes = R.compress(R.pack_matrix(L.w[ri].cpu().numpy(), z, l, DT_I8, threads=threads), DT_I8)
@@ -642,6 +663,22 @@ def cpu_baseline(slsp, torch, layers, xs, outs, out_mode, z, l):
         checked += want.size
         per_layer.append({"layer": L.name, "rows": len(rows), "tokens": len(toks), "lift_s": round(tl, 4),
                           "gemm_s": round(tg, 4)})
+    return R, kind, t_sample, t_total, mism, checked, per_layer
+
+
+def cpu_baseline(slsp, torch, layers, xs, outs, out_mode, z, l):
+    """The GPU arm's cpu_baseline leg: the sampled + extrapolated reference
+    step (rank 0, N = 1), the full o_proj timed once, and — since the sample
+    computes exact reference outputs — the parity check of the GPU outputs of
+    the timed step on the sampled (row, token) blocks."""
+    import numpy as np
+
+    sys.path.insert(0, str(ROOT / "tests"))
+    from oracle_lib import DT_BF16, DT_I8, KIND_INT8, orc, ref
+
+    threads = os.cpu_count() or 1
+    R, kind, t_sample, t_total, mism, checked, per_layer = sampled_reference(slsp, torch, layers, xs, outs,
+                                                                            out_mode, z, l, threads)
     # the full o_proj layer, timed once: calibrates the extrapolation
     o = next((L for L in layers if L.name == "o"), None)
     full = None
