@@ -1877,7 +1877,8 @@ int glift_entry(const void* values, const uint8_t* meta, int64_t n, int64_t kp, 
   p.x_ld = x_ld;
   p.lift_l = l;
   // the 6:8 path loads whole 16-byte source blocks: rows 16-byte aligned
-  if (l == 8 && ((reinterpret_cast<uintptr_t>(x) & 15) || (x_ld & 7))) p.lift_l = -8;
+  // (and the triple layout assumes windows at 0, 2, 4 of each 8-block)
+  if (l == 8 && ((reinterpret_cast<uintptr_t>(x) & 15) || (x_ld & 7) || wc != 3)) p.lift_l = -8;
   p.lift_wc = wc;
   p.lift_windows = windows;
   return run_out_cl<true, MmaKind::F16, kDecodeBN, 1, 2, 0>(out_mode, ta, tb, te, to, p, s, q);

@@ -24,7 +24,9 @@ import paper_2603_05232_b200 as slsp  # noqa: E402
 SHAPES = {"qkv": (4608, 3584), "o": (3584, 3584), "gate_up": (37888, 3584), "down": (3584, 18944),
           "cfg1": (4096, 4096),
           # L2-residency probes: gate_up's K with fewer weight rows (operands fit in L2)
-          "gu4k": (4096, 3584), "gu8k": (8192, 3584), "gu16k": (16384, 3584)}  # BASELINE config 1 (K = N = 4096)
+          "gu4k": (4096, 3584), "gu8k": (8192, 3584), "gu16k": (16384, 3584),
+          # BASELINE config 5: Qwen2.5-14B row shards of 8 GPUs (rounded up to 128 rows)
+          "qkv14s8": (896, 5120), "o14s8": (640, 5120), "gu14s8": (3456, 5120), "down14s8": (640, 13824)}  # BASELINE config 1 (K = N = 4096)
 DENSE_KEYS = {"CLUSTER", "MSUB", "DECODE_M"}
 
 

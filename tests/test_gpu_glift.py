@@ -43,7 +43,7 @@ def test_glift_equals_lift_then_gemm(slsp, n, k, m, out_mode):
     assert torch.equal(got, want)
 
 
-@pytest.mark.parametrize("z,l", [(4, 6), (8, 10), (2, 4)])
+@pytest.mark.parametrize("z,l", [(4, 6), (8, 10), (2, 4), (4, 8)])
 def test_glift_other_patterns(slsp, z, l):
     k = 60 * l * 4
     w, pw, x, _, _ = case(slsp, 640, k, 24, z, l, z * 100 + l)
