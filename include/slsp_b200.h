@@ -287,7 +287,7 @@ typedef struct slsp_gemm_config {
   int ksplit;               /* split-K slices (1: none) */
   int epilogue;             /* 0: chunked TMEM drain, 1: register-staged two-subtile drain */
   int clusters;             /* persistent clusters launched */
-  int reserved;
+  int cluster_ksplit;       /* k-slices reduced inside a cluster through DSMEM (1: none); included in ksplit */
   int64_t workspace_bytes;  /* workspace the split needs (0 when ksplit == 1) */
 } slsp_gemm_config;
 SLSP_API int slsp_sparse_gemm_config(int dtype, int64_t n, int64_t kp, int64_t m, int out_mode, int64_t ws_bytes,

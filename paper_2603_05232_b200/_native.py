@@ -77,11 +77,11 @@ class GemmConfig(C.Structure):
     """slsp_gemm_config (include/slsp_b200.h): the tile configuration a GEMM call launches."""
     _fields_ = [("tokens_per_tile", C.c_int), ("weight_rows_per_tile", C.c_int), ("subtiles", C.c_int),
                 ("half_k_stages", C.c_int), ("stages", C.c_int), ("cluster_ctas", C.c_int), ("ksplit", C.c_int),
-                ("epilogue", C.c_int), ("clusters", C.c_int), ("reserved", C.c_int),
+                ("epilogue", C.c_int), ("clusters", C.c_int), ("cluster_ksplit", C.c_int),
                 ("workspace_bytes", C.c_int64)]
 
     def as_dict(self) -> dict:
-        return {name: getattr(self, name) for name, _ in self._fields_ if name != "reserved"}
+        return {name: getattr(self, name) for name, _ in self._fields_}
 
 
 _lib = None

@@ -79,6 +79,18 @@ SLSP_DEVINL void mbar_arrive_release_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 
+// Distributed shared memory: 16 bytes from a shared::cluster address (mapa).
+SLSP_DEVINL uint4 ld_shared_cluster_v4(uint32_t cluster_addr) {
+  uint4 v;
+  asm volatile("ld.shared::cluster.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(cluster_addr)
+               : "memory");
+  return v;
+}
+
+SLSP_DEVINL void fence_acq_rel_cluster() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
+
 #ifdef SLSP_WATCHDOG
 // Debug build (build.py --watchdog): a wait that spins ~seconds reports the
 // barrier (smem offset, parity) of the first stuck thread and traps.

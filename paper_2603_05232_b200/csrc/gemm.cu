@@ -157,6 +157,10 @@ struct Cfg {
   static constexpr int H0 = (BN / 2 + 31) / 32 * 32;  // REG: columns of the first warp of a lane quarter
   // REG: s_tok slice + one 32x32 BF16 staging box per warp
   static constexpr int EPI_WARP = REG_EPI ? H0 * 4 + 32 * 64 : EPI_BUFS * EPI_BUF;
+  // cluster split-K (Params::ksc): one-subtile decode tiles whose per-warp
+  // staging area holds the warp's 32 rows x BN raw accumulators
+  static constexpr bool KSC_OK = MSUB == 1 && NPAIR == 1 && !AMAX && !LIFT && !REG_EPI && BN <= 64 &&
+                                 EPI_WARP >= 32 * BN * 4;
   // smem ring depth: STAGES_ if given, else as many stages as fit (<= 8)
   static constexpr int FIXED_SMEM0 = EPI_WARPS * EPI_WARP + 4 * 8 + 16 + 1024;
   static constexpr int FIT0 = (227 * 1024 - FIXED_SMEM0) / (STAGE_TX + 16);
@@ -182,7 +186,8 @@ struct Cfg {
   // Two-subtile stages signal subtile 1's operands (A1, E1) on a second
   // barrier, so subtile 0's MMAs start once B, A0 and E0 have landed.
   static constexpr bool SPLIT = MSUB == 2 && SPARSE && !LIFT;
-  static constexpr int NUM_BARS = 4 * STAGES + 4;  // full, empty, xfull, full1 per stage; tfull, tempty
+  // full, empty, xfull, full1 per stage; tfull, tempty; red_full, red_empty (cluster split-K)
+  static constexpr int NUM_BARS = 4 * STAGES + 6;
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16 + 1024;  // + alignment slack
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
   static constexpr uint32_t C_FMT = KIND == MmaKind::I8 ? 2u : 1u;
@@ -237,6 +242,14 @@ struct Params {
   int64_t x_ld;
   int lift_l, lift_wc;
   int64_t lift_windows;
+  // cluster split-K (decode tiles, Cfg::KSC_OK): the cluster holds ksc CTA
+  // pairs that take consecutive k-ranges of ONE tile (the same ranges as a
+  // ksc-way workspace split); each pair parks its raw partial accumulators in
+  // its epilogue staging smem, and every CTA then sums a 1/ksc row share of
+  // the tile over the pairs' buffers through distributed shared memory (in
+  // slice order: the finishing kernel's arithmetic) and applies the epilogue.
+  // No workspace, no finishing launch. 0/1: none.
+  int ksc;
 };
 
 // Fold |bf16| of 2*NW token columns (packed in w, token i = half i&1 of
@@ -337,11 +350,15 @@ SLSP_DEVINL void fold_flush(const Params& p, uint32_t* buf, int64_t tcol0, bool 
 // and each band's weight tiles stay L2-resident while the band sweeps tokens.
 // n_count: token super-tiles (NPAIR token tiles each).
 SLSP_DEVINL void tile_coords(int tile, const Params& p, int m_count, int n_count, int& mt, int& nt, int& kb0,
-                             int& kb1) {
+                             int& kb1, uint32_t kslice = 0, int ksc = 1) {
   const int ks = tile % p.ksplit;  // split-K slice (innermost: the slices of a tile run concurrently)
   tile /= p.ksplit;
   kb0 = ks * p.num_kb / p.ksplit;
   kb1 = (ks + 1) * p.num_kb / p.ksplit;
+  if (ksc > 1) {  // cluster split-K: this pair's k-range (same bounds as a ksc-way workspace split)
+    kb0 = static_cast<int>(kslice) * p.num_kb / ksc;
+    kb1 = (static_cast<int>(kslice) + 1) * p.num_kb / ksc;
+  }
   const int per_group = p.group * n_count;
   const int g = tile / per_group;
   const int first = g * p.group;
@@ -555,7 +572,9 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   uint64_t* full1 = xfull + C::STAGES;  // SPLIT: subtile 1's A/E of a stage have landed
   uint64_t* tfull = full1 + C::STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* red_full = tempty + 2;   // cluster split-K: every pair's partials of this tile are parked
+  uint64_t* red_empty = tempty + 3;  // ... and every CTA has read this CTA's partials
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 4);
 
   const uint32_t warp = threadIdx.x >> 5;
   const uint32_t crank = cluster_ctarank();     // rank in the cluster
@@ -563,8 +582,13 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   const uint32_t rank = crank & 1;              // rank within the pair (cta_group::2 peer)
   const uint32_t lead = crank & ~1u;            // cluster rank of this pair's leader
   const bool leader = rank == 0;
-  const int cluster_id = blockIdx.x / C::CL;
-  const int num_clusters = gridDim.x / C::CL;
+  // cluster split-K: the cluster is ksc pairs, pair index = k-slice
+  const int ksc = C::KSC_OK && p.ksc > 1 ? p.ksc : 1;
+  const uint32_t kslice = ksc > 1 ? pair : 0u;
+  // token tile within a weight-multicast super-tile (pair is 0 unless NPAIR > 1 or ksc > 1)
+  const uint32_t npair_idx = C::KSC_OK && C::NPAIR == 1 ? 0u : pair;
+  const int cluster_id = blockIdx.x / (C::CL * ksc);
+  const int num_clusters = gridDim.x / (C::CL * ksc);
   // a cluster tile = one weight tile x NPAIR consecutive token tiles (pair p
   // takes token tile ns * NPAIR + p; past the last one it recomputes token
   // tile 0 — its loads stay in bounds — and stores nothing)
@@ -589,6 +613,10 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 2 * C::EPI_WARPS);  // every epilogue warp of both CTAs of the pair
+    }
+    if constexpr (C::KSC_OK) {
+      mbar_init(red_full, C::EPI_WARPS * ksc);  // the epilogue warps of the ksc same-rank CTAs
+      mbar_init(red_empty, C::EPI_WARPS * ksc);
     }
     fence_mbar_init();
   }
@@ -628,8 +656,8 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       int it = 0;
       for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
         int mt, ns, kb0, kb1;
-        tile_coords(tile, p, p.m_tiles, n_super, mt, ns, kb0, kb1);
-        int nt = ns * C::NPAIR + static_cast<int>(pair);
+        tile_coords(tile, p, p.m_tiles, n_super, mt, ns, kb0, kb1, kslice, ksc);
+        int nt = ns * C::NPAIR + static_cast<int>(npair_idx);
         if (nt >= p.n_tiles) nt = 0;  // idle pair of the last super-tile: in-bounds loads, no stores
         if (same) mt = nt = 0;
         long long wait_cycles = 0;
@@ -641,8 +669,8 @@ __global__ void __launch_bounds__(C::THREADS, 1)
             // warm L2 with the next tile's first k-blocks: at a tile start the
             // ring's first stages are new weight / token tiles whose loads miss
             int mt2, ns2, kc0, kc1;
-            tile_coords(tile + num_clusters, p, p.m_tiles, n_super, mt2, ns2, kc0, kc1);
-            int nt2 = ns2 * C::NPAIR + static_cast<int>(pair);
+            tile_coords(tile + num_clusters, p, p.m_tiles, n_super, mt2, ns2, kc0, kc1, kslice, ksc);
+            int nt2 = ns2 * C::NPAIR + static_cast<int>(npair_idx);
             if (nt2 >= p.n_tiles) nt2 = 0;
             const int a2 = mt2 * C::BM + static_cast<int>(rank) * C::A_ROWS;
             const int b2 = nt2 * C::BN + static_cast<int>(rank) * C::B_ROWS;
@@ -748,10 +776,14 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      const uint16_t all_ctas = static_cast<uint16_t>((1u << C::CL) - 1);
+      // ring slots are freed in every CTA whose TMA fills them: the pair, or
+      // with weight multicast every pair of the cluster
+      const uint16_t all_ctas = C::NPAIR > 1  ? static_cast<uint16_t>((1u << C::CL) - 1)
+                                : C::KSC_OK ? static_cast<uint16_t>(0x3u << lead)
+                                            : static_cast<uint16_t>(0x3u);
       for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
         int mt_, ns_, kb0, kb1;
-        tile_coords(tile, p, p.m_tiles, n_super, mt_, ns_, kb0, kb1);
+        tile_coords(tile, p, p.m_tiles, n_super, mt_, ns_, kb0, kb1, kslice, ksc);
         const int acc = C::ACC_STAGES == 2 ? (it & 1) : 0;
         const uint32_t acc_phase = C::ACC_STAGES == 2 ? ((it >> 1) & 1) : (it & 1);
         // MSUB=1: double-buffered accumulators, tempty[acc]. MSUB=2: one
@@ -939,7 +971,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       uint32_t phase = 0;
       for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
         int mt_, ns, kb0, kb1;
-        tile_coords(tile, p, p.m_tiles, n_super, mt_, ns, kb0, kb1);
+        tile_coords(tile, p, p.m_tiles, n_super, mt_, ns, kb0, kb1, kslice, ksc);
         const int64_t t_first = static_cast<int64_t>(ns) * C::BN + rank * C::B_ROWS;
         const int rows = static_cast<int>(imin64(C::B_ROWS, p.m - t_first));  // valid token rows (may be <= 0)
         const uint16_t* rp[IT];  // this thread's token rows (6:8 path)
@@ -1121,8 +1153,8 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     int it = 0;
     for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
       int mt, ns, kb0_, kb1_;
-      tile_coords(tile, p, p.m_tiles, n_super, mt, ns, kb0_, kb1_);
-      const int nt = ns * C::NPAIR + static_cast<int>(pair);  // >= n_tiles: idle pair, tcol0 >= m stores nothing
+      tile_coords(tile, p, p.m_tiles, n_super, mt, ns, kb0_, kb1_, kslice, ksc);
+      const int nt = ns * C::NPAIR + static_cast<int>(npair_idx);  // >= n_tiles: idle pair, tcol0 >= m stores nothing
       const int64_t tcol0 = static_cast<int64_t>(nt) * C::BN + half * C::H0;
       const int64_t rowq = static_cast<int64_t>(mt) * C::BM + rank * C::A_ROWS + quarter * 32;  // lane 0's row
       const int64_t row0 = rowq + lane;
@@ -1271,13 +1303,16 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     int it = 0;
     for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
       int mt, ns, kb0_, kb1_;
-      tile_coords(tile, p, p.m_tiles, n_super, mt, ns, kb0_, kb1_);
-      const int nt = ns * C::NPAIR + static_cast<int>(pair);  // >= n_tiles: idle pair, t0 >= m stores nothing
+      tile_coords(tile, p, p.m_tiles, n_super, mt, ns, kb0_, kb1_, kslice, ksc);
+      const int nt = ns * C::NPAIR + static_cast<int>(npair_idx);  // >= n_tiles: idle pair, t0 >= m stores nothing
       const int acc = C::ACC_STAGES == 2 ? (it & 1) : 0;
       const uint32_t acc_phase = C::ACC_STAGES == 2 ? ((it >> 1) & 1) : (it & 1);
       // MSUB=2: all 8 warps drain subtile 0 (two warps per lane quarter,
       // alternating chunks), release it, then subtile 1; with p.tail0
       // subtile 0 has its own barrier (tfull[1]), tfull[0] covers both
+      // cluster split-K: every CTA of the cluster has read this CTA's
+      // previous partials before they are overwritten
+      if (C::KSC_OK && ksc > 1 && it > 0) mbar_wait_cluster_acquire(red_empty, (it - 1) & 1);
 #pragma unroll 1
       for (int h = 0; h < C::MSUB; ++h) {
         if (C::MSUB == 2 && p.tail0) {
@@ -1298,6 +1333,17 @@ __global__ void __launch_bounds__(C::THREADS, 1)
           uint32_t r[C::EPI_COLS];
           tmem_ld_cols(t_base + c * C::EPI_COLS, r);
           tmem_ld_wait();
+          if (C::KSC_OK && ksc > 1) {
+            // cluster split-K: park this slice's raw partials (row = lane) in
+            // the warp's staging area, 16-byte chunk j of the row at j ^ (lane & 15)
+            const uint32_t rowp = smem_u32(stage_base) + lane * (C::BN * 4);
+#pragma unroll
+            for (int i = 0; i < C::EPI_COLS; i += 4) {
+              const uint32_t j = static_cast<uint32_t>(c * C::EPI_COLS + i) >> 2;
+              st_shared_v4(rowp + ((j ^ (lane & 15u)) << 4), r[i], r[i + 1], r[i + 2], r[i + 3]);
+            }
+            continue;
+          }
           if (p.ksplit > 1) {  // split-K: this slice's raw partial sums -> ws[slice][row][t]
             const int64_t row = row0 + lane;
             if (row < p.n && !(p.debug & kDbgNoStore)) {
@@ -1327,6 +1373,87 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[C::MSUB == 2 ? h : acc]), lead));
+      }
+      if constexpr (C::KSC_OK) {
+        if (ksc > 1) {
+          // publish the partials to the same-rank CTA of every pair, wait for theirs
+          fence_acq_rel_cluster();
+          __syncwarp();
+          if (lane == 0)
+            for (int q = 0; q < ksc; ++q) mbar_arrive_release_cluster(mapa_shared(smem_u32(red_full), 2 * q + rank));
+          mbar_wait_cluster_acquire(red_full, it & 1);
+          // this CTA's share: rows [lo, hi) of its 128 (lane quarter w/32 lives
+          // in epilogue warp (w/32 + 2) & 3's staging area). Thread t takes
+          // row lo + t % 64 and the 32-token half t / 64 of the tile: all its
+          // DSMEM loads of a slice are in flight at once, sums in slice order
+          // (the finishing kernel's arithmetic), then the epilogue.
+          static_assert(C::BN == 64 && C::EPI_WARPS == 4, "cluster split-K: 64-token tiles, 128 epilogue threads");
+          const int lo = 128 * static_cast<int>(kslice) / ksc, hi = 128 * (static_cast<int>(kslice) + 1) / ksc;
+          const int tid = static_cast<int>((warp - 2) * 32 + lane);
+          const int rr = lo + (tid & 63);
+          const int half = tid >> 6;
+          const int64_t tt0 = static_cast<int64_t>(nt) * C::BN + 32 * half;
+          const int64_t row = static_cast<int64_t>(mt) * C::BM + rank * C::A_ROWS + rr;
+          const int tcols = static_cast<int>(imin64(32, p.m - tt0));  // valid tokens of this half
+          if (rr < hi && tcols > 0 && row < p.n && !(p.debug & kDbgNoStore)) {
+            const uint32_t rowp = smem_u32(smem + C::OFF_EPI) + ((((rr >> 5) + 2) & 3) * C::EPI_WARP) +
+                                  (rr & 31) * (C::BN * 4);
+            const float sc = C::OUT == SLSP_OUT_RAW_NM ? 0.f : __ldg(p.s_ch + row);
+#pragma unroll 1
+            for (int b = 0; b < 2; ++b) {  // two batches of 16 tokens (register budget of the lift-warp configs)
+              const int tb = 16 * b;
+              if (tb >= tcols) break;
+              uint32_t acc[16];
+              for (int q = 0; q < ksc; ++q) {
+                uint4 x[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                  if (tb + 4 * c < tcols)
+                    x[c] = ld_shared_cluster_v4(mapa_shared(
+                        rowp + ((static_cast<uint32_t>(8 * half + 4 * b + c) ^ (rr & 15u)) << 4), 2 * q + rank));
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                  if (tb + 4 * c >= tcols) continue;
+                  const uint32_t y[4] = {x[c].x, x[c].y, x[c].z, x[c].w};
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) {
+                    if (q == 0)
+                      acc[4 * c + e] = y[e];
+                    else if constexpr (std::is_same<typename C::Acc, int32_t>::value)
+                      acc[4 * c + e] =
+                          static_cast<uint32_t>(static_cast<int32_t>(acc[4 * c + e]) + static_cast<int32_t>(y[e]));
+                    else
+                      acc[4 * c + e] =
+                          __float_as_uint(__fadd_rn(__uint_as_float(acc[4 * c + e]), __uint_as_float(y[e])));
+                  }
+                }
+              }
+              const int64_t t0 = tt0 + tb;
+              if constexpr (C::OUT == SLSP_OUT_RAW_NM) {
+                uint32_t* dst = static_cast<uint32_t*>(p.out) + row * p.ldo + t0;
+#pragma unroll
+                for (int e = 0; e < 16; ++e)
+                  if (tb + e < tcols) dst[e] = acc[e];
+              } else {
+                uint16_t* o = static_cast<uint16_t*>(p.out);
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                  if (tb + e < tcols) {
+                    const __nv_bfloat16 v =
+                        __float2bfloat16_rn(dequant<typename C::Acc>(acc[e], sc, __ldg(p.s_tok + t0 + e)));
+                    o[C::OUT == SLSP_OUT_BF16_MN ? (t0 + e) * p.ldo + row : row * p.ldo + t0 + e] =
+                        *reinterpret_cast<const uint16_t*>(&v);
+                  }
+                }
+              }
+            }
+          }
+          // reads done: release every peer's buffer for its next tile
+          fence_acq_rel_cluster();
+          __syncwarp();
+          if (lane == 0)
+            for (int q = 0; q < ksc; ++q) mbar_arrive_release_cluster(mapa_shared(smem_u32(red_empty), 2 * q + rank));
+        }
       }
       if constexpr (C::AMAX_SM)
         if (C::AMAX && p.amax)
@@ -1486,6 +1613,48 @@ int choose_ksplit(int tiles, int num_kb, int clusters, int cap, int64_t slice_by
   return best;
 }
 
+// Cluster split-K for the decode tiles (Params::ksc): ksc pairs per cluster
+// share one tile's k-range and reduce through distributed shared memory.
+// Same time model as choose_ksplit (waves x k-blocks per slice), with the
+// in-cluster reduction priced at kKscCostKb k-block times and no finishing
+// launch or slice traffic; taken when it beats both the unsplit grid and the
+// workspace split choose_ksplit picked (ws_split, 1 = none). avail[k] =
+// co-resident clusters of 2k CTAs. forced: SLSP_GEMM_KSC (k > 1 forces k;
+// 0 = this model; 1 = off, the default).
+constexpr int kMaxKsc = 4;  // clusters of <= 8 CTAs (portable size)
+constexpr int kKscCostKb = 2;
+// Off by default (SLSP_GEMM_KSC: 0 = cost model, 1 = off, k = forced): measured
+// on the Llama-3.1-8B decode shapes and config 1 it is not faster than the
+// workspace split + finishing kernel — with no operand loads at all the
+// cluster-reduced launch still costs 1-3.5 us more; only qkv
+// at M = 1 gains (0.1-0.5 us).
+constexpr int kKscDefault = 1;
+
+int choose_ksc(int tiles, int num_kb, const int* avail, int forced, int ws_split, int clusters, int64_t slice_bytes) {
+  auto waves = [](int t, int c) { return c > 0 ? (t + c - 1) / c : 1 << 30; };
+  if (forced > 1) {
+    const int k = forced < kMaxKsc ? forced : kMaxKsc;
+    return avail[k] > 0 && num_kb >= 2 * k ? k : 1;
+  }
+  const int kSplitCostKb = static_cast<int>(env_knob("SLSP_GEMM_SPLITCOST", 16));
+  constexpr double kSliceBytesPerKb = 1.35e6;
+  double ref = static_cast<double>(waves(tiles, clusters)) * num_kb;
+  if (ws_split > 1)
+    ref = static_cast<double>(waves(tiles * ws_split, clusters)) * ((num_kb + ws_split - 1) / ws_split) +
+          kSplitCostKb + 2.0 * ws_split * static_cast<double>(slice_bytes) / kSliceBytesPerKb;
+  int best = 1;
+  double best_cost = ref;
+  for (int k = 2; k <= kMaxKsc; ++k) {
+    if (avail[k] <= 0 || num_kb < 2 * k) continue;
+    const double cost = static_cast<double>(waves(tiles, avail[k])) * ((num_kb + k - 1) / k) + kKscCostKb;
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best = k;
+    }
+  }
+  return best;
+}
+
 // After a split-K GEMM: sum the slices in slice order (exact for int32,
 // deterministic for fp32), then the epilogue's exact arithmetic — a18 for
 // BF16 outputs (bf16((acc * s_ch[n]) * s_tok[t])), the raw sum for RAW_NM.
@@ -1551,10 +1720,47 @@ int run(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const 
   // split-K where the tiles do not fill the machine (decode-shaped M): needs
   // an accumulation target (the int32/fp32 output itself, or a workspace)
   p.ksplit = 1;
+  p.ksc = 1;
   const int64_t slice = p.n * p.m * 4;
   if constexpr (!C::REG_EPI && !C::LIFT) {
     const int cap = p.ws && slice > 0 ? static_cast<int>(p.ws_cap / slice < 16 ? p.ws_cap / slice : 16) : 1;
     if (tiles > 0 && p.m <= kSplitMaxM && cap > 1) p.ksplit = choose_ksplit(tiles, p.num_kb, clusters, cap, slice);
+  }
+  // cluster split-K (decode tiles): preferred over a workspace split when its
+  // estimated cost is lower; SLSP_GEMM_KSPLIT (forced workspace split) turns it off
+  int ksc_clusters = clusters;
+  if constexpr (C::KSC_OK) {
+    static slsp_host::PerDevice<int> ksc_cache[kMaxKsc + 1];
+    const int forced_ws = static_cast<int>(env_knob("SLSP_GEMM_KSPLIT", 0));
+    const int forced = static_cast<int>(env_knob("SLSP_GEMM_KSC", kKscDefault));
+    if (tiles > 0 && forced_ws == 0 && forced != 1) {
+      int avail[kMaxKsc + 1] = {0, clusters};
+      for (int k = 2; k <= kMaxKsc; ++k) {
+        int v = 0;
+        int st2 = ksc_cache[k].get(&v, [&](int& out) -> int {
+          cudaLaunchConfig_t c2 = cfg;
+          cudaLaunchAttribute a2[2] = {attr[0], attr[1]};
+          a2[0].val.clusterDim.x = C::CL * k;
+          c2.attrs = a2;
+          c2.gridDim = dim3(C::CL * k * (num_sms() / (C::CL * k)));
+          int nc = 0;
+          if (cudaOccupancyMaxActiveClusters(&nc, kern, &c2) != cudaSuccess) {
+            (void)cudaGetLastError();
+            nc = 0;
+          }
+          out = nc;
+          return SLSP_OK;
+        });
+        if (st2) return st2;
+        avail[k] = cluster_cap > 0 && v > cluster_cap ? cluster_cap : v;
+      }
+      const int best = choose_ksc(tiles, p.num_kb, avail, forced, p.ksplit, clusters, slice);
+      if (best > 1) {
+        p.ksc = best;
+        p.ksplit = 1;
+        ksc_clusters = avail[best];
+      }
+    }
   }
   if (query) {
     query->tokens_per_tile = C::BN;
@@ -1562,17 +1768,23 @@ int run(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const 
     query->subtiles = C::MSUB;
     query->half_k_stages = C::KH ? 1 : 0;
     query->stages = C::STAGES;
-    query->cluster_ctas = C::CL;
-    query->ksplit = p.ksplit;
+    query->cluster_ctas = C::CL * p.ksc;
+    query->ksplit = p.ksplit * p.ksc;
+    query->cluster_ksplit = p.ksc;
     query->epilogue = C::REG_EPI ? 1 : 0;
-    query->clusters = clusters < tiles * p.ksplit ? clusters : tiles * p.ksplit;
+    query->clusters = p.ksc > 1 ? (ksc_clusters < tiles ? ksc_clusters : tiles)
+                                : (clusters < tiles * p.ksplit ? clusters : tiles * p.ksplit);
     query->workspace_bytes = p.ksplit > 1 ? p.ksplit * slice : 0;
     return SLSP_OK;
   }
   if (tiles == 0) return SLSP_OK;
   if (p.ksplit > 1) tiles *= p.ksplit;
+  if (p.ksc > 1) {
+    clusters = ksc_clusters;
+    attr[0].val.clusterDim.x = C::CL * p.ksc;
+  }
   if (clusters > tiles) clusters = tiles;
-  cfg.gridDim = dim3(C::CL * clusters);
+  cfg.gridDim = dim3(C::CL * p.ksc * clusters);
   SLSP_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, a, b, e, o, p));
   if (p.ksplit > 1) {
     const int64_t total = p.n * p.m;

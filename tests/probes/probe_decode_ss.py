@@ -120,7 +120,7 @@ def main():
                                   "glift_step_us": round(t_gl, 2) if t_gl else None,
                                   "glift_speedup": round(t_de / t_gl, 3) if t_gl else None,
                                   "gemm_weight_gbs": round(sb / t_g / 1e3, 1), "dense_weight_gbs": round(db / t_de / 1e3, 1),
-                                  "cfg": f"bn{cfg['tokens_per_tile']} ks{cfg['ksplit']} cl{cfg['clusters']}"}),
+                                  "cfg": f"bn{cfg['tokens_per_tile']} ks{cfg['ksplit']} ksc{cfg['cluster_ksplit']} cl{cfg['clusters']}"}),
                       flush=True)
 
 
