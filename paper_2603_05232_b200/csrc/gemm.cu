@@ -1379,71 +1379,97 @@ __global__ void __launch_bounds__(C::THREADS, 1)
           // publish the partials to the same-rank CTA of every pair, wait for theirs
           fence_acq_rel_cluster();
           __syncwarp();
+          // (the cluster-scope fence above is the release; plain remote
+          // arrives — .release.cluster would fence again per arrive)
           if (lane == 0)
-            for (int q = 0; q < ksc; ++q) mbar_arrive_release_cluster(mapa_shared(smem_u32(red_full), 2 * q + rank));
+            for (int q = 0; q < ksc; ++q) mbar_arrive_cluster(mapa_shared(smem_u32(red_full), 2 * q + rank));
           mbar_wait_cluster_acquire(red_full, it & 1);
           // this CTA's share: rows [lo, hi) of its 128 (lane quarter w/32 lives
-          // in epilogue warp (w/32 + 2) & 3's staging area). Thread t takes
-          // row lo + t % 64 and the 32-token half t / 64 of the tile: all its
-          // DSMEM loads of a slice are in flight at once, sums in slice order
-          // (the finishing kernel's arithmetic), then the epilogue.
+          // in epilogue warp (w/32 + 2) & 3's staging area), 16-byte chunks
+          // (4 tokens) as units: [N][M] outputs take chunks fastest (a warp
+          // stores whole rows, coalesced), [M][N] rows fastest. Each thread
+          // keeps 4 units' DSMEM loads of a slice in flight, sums in slice
+          // order (the finishing kernel's arithmetic), applies the epilogue.
           static_assert(C::BN == 64 && C::EPI_WARPS == 4, "cluster split-K: 64-token tiles, 128 epilogue threads");
+          constexpr bool kRowsFast = C::OUT == SLSP_OUT_BF16_MN;
           const int lo = 128 * static_cast<int>(kslice) / ksc, hi = 128 * (static_cast<int>(kslice) + 1) / ksc;
           const int tid = static_cast<int>((warp - 2) * 32 + lane);
-          const int rr = lo + (tid & 63);
-          const int half = tid >> 6;
-          const int64_t tt0 = static_cast<int64_t>(nt) * C::BN + 32 * half;
-          const int64_t row = static_cast<int64_t>(mt) * C::BM + rank * C::A_ROWS + rr;
-          const int tcols = static_cast<int>(imin64(32, p.m - tt0));  // valid tokens of this half
-          if (rr < hi && tcols > 0 && row < p.n && !(p.debug & kDbgNoStore)) {
-            const uint32_t rowp = smem_u32(smem + C::OFF_EPI) + ((((rr >> 5) + 2) & 3) * C::EPI_WARP) +
-                                  (rr & 31) * (C::BN * 4);
-            const float sc = C::OUT == SLSP_OUT_RAW_NM ? 0.f : __ldg(p.s_ch + row);
+          const int64_t tt0 = static_cast<int64_t>(nt) * C::BN;
+          const int tcols = static_cast<int>(imin64(C::BN, p.m - tt0));  // valid tokens of the tile
+          const int64_t row_base = static_cast<int64_t>(mt) * C::BM + rank * C::A_ROWS;
+          const uint32_t epi0 = smem_u32(smem + C::OFF_EPI);
+          constexpr int ESZ = C::OUT == SLSP_OUT_RAW_NM ? 4 : 2;
+          const bool vec = (reinterpret_cast<uintptr_t>(p.out) % 16 == 0) && ((p.ldo * ESZ) % 16 == 0);
 #pragma unroll 1
-            for (int b = 0; b < 2; ++b) {  // two batches of 16 tokens (register budget of the lift-warp configs)
-              const int tb = 16 * b;
-              if (tb >= tcols) break;
-              uint32_t acc[16];
-              for (int q = 0; q < ksc; ++q) {
-                uint4 x[4];
+          for (int u0 = 0; u0 < 1024; u0 += 4 * 128) {  // 64 rows x 16 chunks, 4 units per thread per batch
+            uint32_t acc[4][4];
+            int rr[4], jj[4];
+            bool ok[4];
 #pragma unroll
-                for (int c = 0; c < 4; ++c)
-                  if (tb + 4 * c < tcols)
-                    x[c] = ld_shared_cluster_v4(mapa_shared(
-                        rowp + ((static_cast<uint32_t>(8 * half + 4 * b + c) ^ (rr & 15u)) << 4), 2 * q + rank));
+            for (int b = 0; b < 4; ++b) {
+              const int u = u0 + b * 128 + tid;
+              const int ro = kRowsFast ? (u & 63) : (u >> 4);
+              jj[b] = kRowsFast ? (u >> 6) : (u & 15);
+              rr[b] = lo + ro;
+              ok[b] = rr[b] < hi && 4 * jj[b] < tcols && row_base + rr[b] < p.n;
+            }
+            for (int q = 0; q < ksc; ++q) {
+              uint4 x[4];
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                  if (tb + 4 * c >= tcols) continue;
-                  const uint32_t y[4] = {x[c].x, x[c].y, x[c].z, x[c].w};
+              for (int b = 0; b < 4; ++b)
+                if (ok[b])
+                  x[b] = ld_shared_cluster_v4(mapa_shared(
+                      epi0 + ((((rr[b] >> 5) + 2) & 3) * C::EPI_WARP) + (rr[b] & 31) * (C::BN * 4) +
+                          ((static_cast<uint32_t>(jj[b]) ^ (static_cast<uint32_t>(rr[b]) & 15u)) << 4),
+                      2 * q + rank));
 #pragma unroll
-                  for (int e = 0; e < 4; ++e) {
-                    if (q == 0)
-                      acc[4 * c + e] = y[e];
-                    else if constexpr (std::is_same<typename C::Acc, int32_t>::value)
-                      acc[4 * c + e] =
-                          static_cast<uint32_t>(static_cast<int32_t>(acc[4 * c + e]) + static_cast<int32_t>(y[e]));
-                    else
-                      acc[4 * c + e] =
-                          __float_as_uint(__fadd_rn(__uint_as_float(acc[4 * c + e]), __uint_as_float(y[e])));
-                  }
+              for (int b = 0; b < 4; ++b) {
+                if (!ok[b]) continue;
+                const uint32_t y[4] = {x[b].x, x[b].y, x[b].z, x[b].w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  if (q == 0)
+                    acc[b][e] = y[e];
+                  else if constexpr (std::is_same<typename C::Acc, int32_t>::value)
+                    acc[b][e] = static_cast<uint32_t>(static_cast<int32_t>(acc[b][e]) + static_cast<int32_t>(y[e]));
+                  else
+                    acc[b][e] = __float_as_uint(__fadd_rn(__uint_as_float(acc[b][e]), __uint_as_float(y[e])));
                 }
               }
-              const int64_t t0 = tt0 + tb;
+            }
+            if (p.debug & kDbgNoStore) continue;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              if (!ok[b]) continue;
+              const int64_t row = row_base + rr[b];
+              const int64_t t = tt0 + 4 * jj[b];
+              const int ne = tcols - 4 * jj[b];  // >= 1
               if constexpr (C::OUT == SLSP_OUT_RAW_NM) {
-                uint32_t* dst = static_cast<uint32_t*>(p.out) + row * p.ldo + t0;
+                uint32_t* dst = static_cast<uint32_t*>(p.out) + row * p.ldo + t;
+                if (ne >= 4 && vec) {
+                  *reinterpret_cast<uint4*>(dst) = make_uint4(acc[b][0], acc[b][1], acc[b][2], acc[b][3]);
+                } else {
 #pragma unroll
-                for (int e = 0; e < 16; ++e)
-                  if (tb + e < tcols) dst[e] = acc[e];
+                  for (int e = 0; e < 4; ++e)
+                    if (e < ne) dst[e] = acc[b][e];
+                }
               } else {
-                uint16_t* o = static_cast<uint16_t*>(p.out);
+                const float sc = __ldg(p.s_ch + row);
+                uint16_t h[4];
 #pragma unroll
-                for (int e = 0; e < 16; ++e) {
-                  if (tb + e < tcols) {
-                    const __nv_bfloat16 v =
-                        __float2bfloat16_rn(dequant<typename C::Acc>(acc[e], sc, __ldg(p.s_tok + t0 + e)));
-                    o[C::OUT == SLSP_OUT_BF16_MN ? (t0 + e) * p.ldo + row : row * p.ldo + t0 + e] =
-                        *reinterpret_cast<const uint16_t*>(&v);
-                  }
+                for (int e = 0; e < 4; ++e) {
+                  const __nv_bfloat16 v = __float2bfloat16_rn(
+                      dequant<typename C::Acc>(acc[b][e], sc, e < ne ? __ldg(p.s_tok + t + e) : 0.f));
+                  h[e] = *reinterpret_cast<const uint16_t*>(&v);
+                }
+                uint16_t* o = static_cast<uint16_t*>(p.out);
+                if (C::OUT == SLSP_OUT_BF16_NM && ne >= 4 && vec) {
+                  *reinterpret_cast<uint2*>(o + row * p.ldo + t) =
+                      make_uint2(h[0] | (static_cast<uint32_t>(h[1]) << 16), h[2] | (static_cast<uint32_t>(h[3]) << 16));
+                } else {
+#pragma unroll
+                  for (int e = 0; e < 4; ++e)
+                    if (e < ne) o[C::OUT == SLSP_OUT_BF16_MN ? (t + e) * p.ldo + row : row * p.ldo + t + e] = h[e];
                 }
               }
             }
@@ -1452,7 +1478,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
           fence_acq_rel_cluster();
           __syncwarp();
           if (lane == 0)
-            for (int q = 0; q < ksc; ++q) mbar_arrive_release_cluster(mapa_shared(smem_u32(red_empty), 2 * q + rank));
+            for (int q = 0; q < ksc; ++q) mbar_arrive_cluster(mapa_shared(smem_u32(red_empty), 2 * q + rank));
         }
       }
       if constexpr (C::AMAX_SM)
@@ -1620,15 +1646,14 @@ int choose_ksplit(int tiles, int num_kb, int clusters, int cap, int64_t slice_by
 // launch or slice traffic; taken when it beats both the unsplit grid and the
 // workspace split choose_ksplit picked (ws_split, 1 = none). avail[k] =
 // co-resident clusters of 2k CTAs. forced: SLSP_GEMM_KSC (k > 1 forces k;
-// 0 = this model; 1 = off, the default).
+// 0 = this model, the default; 1 = off).
 constexpr int kMaxKsc = 4;  // clusters of <= 8 CTAs (portable size)
-constexpr int kKscCostKb = 2;
-// Off by default (SLSP_GEMM_KSC: 0 = cost model, 1 = off, k = forced): measured
-// on the Llama-3.1-8B decode shapes and config 1 it is not faster than the
-// workspace split + finishing kernel — with no operand loads at all the
-// cluster-reduced launch still costs 1-3.5 us more; only qkv
-// at M = 1 gains (0.1-0.5 us).
-constexpr int kKscDefault = 1;
+// price of the in-cluster reduction in k-block times, fitted to the decode
+// measurements: down M=1 keeps the 4-way workspace split,
+// down M=64 and the qkv / o / config-1 shapes take the cluster split
+constexpr int kKscCostKb = 4;
+// SLSP_GEMM_KSC: 0 = the cost model (default), 1 = off, k > 1 = forced
+constexpr int kKscDefault = 0;
 
 int choose_ksc(int tiles, int num_kb, const int* avail, int forced, int ws_split, int clusters, int64_t slice_bytes) {
   auto waves = [](int t, int c) { return c > 0 ? (t + c - 1) / c : 1 << 30; };

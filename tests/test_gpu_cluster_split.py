@@ -91,16 +91,16 @@ def test_bf16_cluster_split_equals_workspace_split(slsp, n, k, m, ksc):
     assert torch.all((got - ref).abs() <= tol)
 
 
-def test_cluster_split_default_off_and_model(slsp):
-    """Default: off (measured not faster); SLSP_GEMM_KSC=0 asks
-    the cost model, which takes it for decode shapes whose tiles leave
-    clusters idle and never at large M."""
+def test_cluster_split_cost_model(slsp):
+    """Default (cost model): decode shapes whose tiles leave clusters idle take
+    the cluster split (no workspace), large M never does; SLSP_GEMM_KSC=1
+    turns it off."""
     g = torch.Generator(device="cuda").manual_seed(7)
     w = slsp.magnitude_prune(torch.randint(-127, 128, (4096, 4096), dtype=torch.int8, device="cuda", generator=g), 6, 8)
     pw = slsp.pack_compress(w, 6, 8)
-    assert slsp.sparse_gemm_config(pw, 128, slsp.OUT_BF16_NM)["cluster_ksplit"] == 1
-    with slsp.knobs(SLSP_GEMM_KSC="0"):
-        c1 = slsp.sparse_gemm_config(pw, 128, slsp.OUT_BF16_NM)
-        assert c1["cluster_ksplit"] > 1 and c1["workspace_bytes"] == 0, c1
-        c2 = slsp.sparse_gemm_config(pw, 8192, slsp.OUT_BF16_NM)
-        assert c2["cluster_ksplit"] == 1 and c2["ksplit"] == 1, c2
+    c1 = slsp.sparse_gemm_config(pw, 128, slsp.OUT_BF16_NM)
+    assert c1["cluster_ksplit"] > 1 and c1["workspace_bytes"] == 0, c1
+    c2 = slsp.sparse_gemm_config(pw, 8192, slsp.OUT_BF16_NM)
+    assert c2["cluster_ksplit"] == 1 and c2["ksplit"] == 1, c2
+    with slsp.knobs(SLSP_GEMM_KSC="1"):
+        assert slsp.sparse_gemm_config(pw, 128, slsp.OUT_BF16_NM)["cluster_ksplit"] == 1
