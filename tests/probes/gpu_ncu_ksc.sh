@@ -1,8 +1,12 @@
-cd ${GRAFT_REPO_ROOT:-.}; mkdir -p gpurun_out
+#!/bin/bash
+# ncu --set full of the decode GEMMs with and without the cluster split-K
+# (config 1 INT8 M=128; Llama-3.1-8B qkv BF16 M=1), summaries into gpurun_out.
+cd ${GRAFT_REPO_ROOT:-.}; mkdir -p gpurun_out /tmp/ncu
 NCU="ncu --set full --clock-control none --import-source on"
-for k in 1 2; do
-  SLSP_GEMM_KSC=$k timeout 300 $NCU -k regex:gemm_kernel -s 2 -c 1 -o gpurun_out/ksc_cfg1_$k python tests/probes/probe_ncu_targets.py cfg1_sparse > gpurun_out/ncu_ksc_$k.log 2>&1
+for t in cfg1_sparse cfg1_dense dec_sparse dec_dense; do
+  for k in 0 1; do
+    SLSP_GEMM_KSC=$k timeout 300 $NCU -k regex:gemm_kernel -s 2 -c 1 -o /tmp/ncu/r02_ksc${k}_$t python tests/probes/probe_ncu_targets.py $t > /tmp/ncu/ksc${k}_$t.log 2>&1
+  done
 done
-SLSP_GEMM_KSC=1 timeout 120 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:gemm_kernel python tests/probes/probe_ncu_targets.py cfg1_sparse > gpurun_out/t1.log 2>&1
-SLSP_GEMM_KSC=2 timeout 120 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:gemm_kernel python tests/probes/probe_ncu_targets.py cfg1_sparse > gpurun_out/t2.log 2>&1
-ls -la gpurun_out
+python tests/ncu_summary.py /tmp/ncu/r02_ksc*.ncu-rep > gpurun_out/r02_ncu_ksc.txt 2>&1
+tail -n 1 /tmp/ncu/*.log
