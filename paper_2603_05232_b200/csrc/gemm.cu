@@ -1641,43 +1641,42 @@ int choose_ksplit(int tiles, int num_kb, int clusters, int cap, int64_t slice_by
 
 // Cluster split-K for the decode tiles (Params::ksc): ksc pairs per cluster
 // share one tile's k-range and reduce through distributed shared memory.
-// Same time model as choose_ksplit (waves x k-blocks per slice), with the
-// in-cluster reduction priced at kKscCostKb k-block times and no finishing
-// launch or slice traffic; taken when it beats both the unsplit grid and the
-// workspace split choose_ksplit picked (ws_split, 1 = none). avail[k] =
-// co-resident clusters of 2k CTAs. forced: SLSP_GEMM_KSC (k > 1 forces k;
-// 0 = this model, the default; 1 = off).
 constexpr int kMaxKsc = 4;  // clusters of <= 8 CTAs (portable size)
-// price of the in-cluster reduction in k-block times, fitted to the decode
-// measurements: down M=1 keeps the 4-way workspace split,
-// down M=64 and the qkv / o / config-1 shapes take the cluster split
-constexpr int kKscCostKb = 4;
-// SLSP_GEMM_KSC: 0 = the cost model (default), 1 = off, k > 1 = forced
 constexpr int kKscDefault = 0;
 
-int choose_ksc(int tiles, int num_kb, const int* avail, int forced, int ws_split, int clusters, int64_t slice_bytes) {
+// Decode tiles: one model over {unsplit, workspace split sp, cluster split
+// k}, in k-block times per CTA pair: waves x k-blocks per slice + a fixed
+// price (4 for either split: the finishing kernel is PDL-launched beside the
+// GEMM and starts the moment the slices land) + for the workspace split its
+// slices' write + read traffic, weighted 3x the moderate-M model's (fitted to
+// the Llama-3.1-8B decode shapes and config 1: o / down keep
+// the 4-way workspace split at M = 1 and take the cluster split at M = 64,
+// qkv likewise, config 1 the cluster split, gate_up 7-way / unsplit).
+void choose_decode_split(int tiles, int num_kb, int clusters, int ws_cap, int64_t slice_bytes, const int* avail,
+                         int& ksplit, int& ksc) {
   auto waves = [](int t, int c) { return c > 0 ? (t + c - 1) / c : 1 << 30; };
-  if (forced > 1) {
-    const int k = forced < kMaxKsc ? forced : kMaxKsc;
-    return avail[k] > 0 && num_kb >= 2 * k ? k : 1;
-  }
-  const int kSplitCostKb = static_cast<int>(env_knob("SLSP_GEMM_SPLITCOST", 16));
-  constexpr double kSliceBytesPerKb = 1.35e6;
-  double ref = static_cast<double>(waves(tiles, clusters)) * num_kb;
-  if (ws_split > 1)
-    ref = static_cast<double>(waves(tiles * ws_split, clusters)) * ((num_kb + ws_split - 1) / ws_split) +
-          kSplitCostKb + 2.0 * ws_split * static_cast<double>(slice_bytes) / kSliceBytesPerKb;
-  int best = 1;
-  double best_cost = ref;
-  for (int k = 2; k <= kMaxKsc; ++k) {
-    if (avail[k] <= 0 || num_kb < 2 * k) continue;
-    const double cost = static_cast<double>(waves(tiles, avail[k])) * ((num_kb + k - 1) / k) + kKscCostKb;
-    if (cost < best_cost - 1e-9) {
-      best_cost = cost;
-      best = k;
+  constexpr double kPrice = 4.0, kSliceBytesPerKb = 1.35e6 / 3.0;
+  double best = static_cast<double>(waves(tiles, clusters)) * num_kb;
+  ksplit = 1;
+  ksc = 1;
+  const int hi = ws_cap < num_kb / 2 ? ws_cap : num_kb / 2;
+  for (int sp = 2; sp <= hi; ++sp) {
+    const double c = static_cast<double>(waves(tiles * sp, clusters)) * ((num_kb + sp - 1) / sp) + kPrice +
+                     2.0 * sp * static_cast<double>(slice_bytes) / kSliceBytesPerKb;
+    if (c < best - 1e-9) {
+      best = c;
+      ksplit = sp;
     }
   }
-  return best;
+  for (int k = 2; k <= kMaxKsc; ++k) {
+    if (avail[k] <= 0 || num_kb < 2 * k) continue;
+    const double c = static_cast<double>(waves(tiles, avail[k])) * ((num_kb + k - 1) / k) + kPrice;
+    if (c < best - 1e-9) {
+      best = c;
+      ksplit = 1;
+      ksc = k;
+    }
+  }
 }
 
 // After a split-K GEMM: sum the slices in slice order (exact for int32,
@@ -1687,6 +1686,10 @@ template <typename Acc, int OUT>
 __global__ void splitk_finish_kernel(const Acc* __restrict__ ws, int slices, int64_t n, int64_t m,
                                      const float* __restrict__ s_ch, const float* __restrict__ s_tok, void* out,
                                      int64_t ldo) {
+  // PDL: the blocks are resident beside the GEMM's CTAs (no shared memory)
+  // and start the moment its slices are complete and visible
+  pdl_wait();
+  pdl_trigger();
   const int64_t total = n * m;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -1779,12 +1782,17 @@ int run(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const 
         if (st2) return st2;
         avail[k] = cluster_cap > 0 && v > cluster_cap ? cluster_cap : v;
       }
-      const int best = choose_ksc(tiles, p.num_kb, avail, forced, p.ksplit, clusters, slice);
-      if (best > 1) {
-        p.ksc = best;
-        p.ksplit = 1;
-        ksc_clusters = avail[best];
+      if (forced > 1) {  // forced cluster split (when it fits)
+        const int k = forced < kMaxKsc ? forced : kMaxKsc;
+        if (avail[k] > 0 && p.num_kb >= 2 * k) {
+          p.ksc = k;
+          p.ksplit = 1;
+        }
+      } else {
+        const int cap = p.ws && slice > 0 ? static_cast<int>(p.ws_cap / slice < 16 ? p.ws_cap / slice : 16) : 1;
+        choose_decode_split(tiles, p.num_kb, clusters, cap, slice, avail, p.ksplit, p.ksc);
       }
+      if (p.ksc > 1) ksc_clusters = avail[p.ksc];
     }
   }
   if (query) {
@@ -1814,9 +1822,10 @@ int run(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& e, const 
   if (p.ksplit > 1) {
     const int64_t total = p.n * p.m;
     const unsigned grid = static_cast<unsigned>((total + 255) / 256 < 148 * 16 ? (total + 255) / 256 : 148 * 16);
-    splitk_finish_kernel<typename C::Acc, C::OUT><<<grid, 256, 0, s>>>(
-        static_cast<const typename C::Acc*>(p.ws), p.ksplit, p.n, p.m, p.s_ch, p.s_tok, p.out, p.ldo);
-    SLSP_CUDA_TRY(cudaGetLastError());
+    const int st2 = slsp_host::launch_pdl(p.m, splitk_finish_kernel<typename C::Acc, C::OUT>, dim3(grid), dim3(256), 0,
+                                          s, static_cast<const typename C::Acc*>(p.ws), p.ksplit, p.n, p.m, p.s_ch,
+                                          p.s_tok, p.out, p.ldo);
+    if (st2) return st2;
   }
   return SLSP_OK;
 }
