@@ -104,3 +104,32 @@ def test_cluster_split_cost_model(slsp):
     assert c2["cluster_ksplit"] == 1 and c2["ksplit"] == 1, c2
     with slsp.knobs(SLSP_GEMM_KSC="1"):
         assert slsp.sparse_gemm_config(pw, 128, slsp.OUT_BF16_NM)["cluster_ksplit"] == 1
+
+
+@pytest.mark.parametrize("m", [1, 16, 64])
+@pytest.mark.parametrize("ksc", [2, 4])
+def test_fp8_cluster_split_equals_workspace_split(slsp, m, ksc):
+    """FP8 (e4m3 weights and lifted activations, fp32 accumulators): cluster
+    split == workspace split of the same slice count, bit for bit, in every
+    output mode."""
+    g = torch.Generator(device="cuda").manual_seed(100 + m + ksc)
+    n, k = 2048, 4096
+    w = slsp.magnitude_prune(((torch.rand(n, k, device="cuda", generator=g) * 2 - 1) * 200).to(torch.float8_e4m3fn),
+                             6, 8)
+    pw = slsp.pack_compress(w, 6, 8)
+    x = (torch.rand(m, k, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    payload, s_tok = slsp.fused_quant_slide(x, 6, 8, kind=slsp.QUANT_FP8E4M3)
+    s_ch = torch.rand(n, device="cuda", generator=g) * 0.01 + 0.001
+    outs = {}
+    for tag, kn in (("cl", {"SLSP_GEMM_KSC": str(ksc)}), ("ws", {"SLSP_GEMM_KSPLIT": str(ksc)})):
+        with slsp.knobs(**kn):
+            cfg = slsp.sparse_gemm_config(pw, m, slsp.OUT_BF16_NM)
+            assert cfg["ksplit"] == ksc and cfg["cluster_ksplit"] == (ksc if tag == "cl" else 1), (tag, cfg)
+            for mode in (slsp.OUT_RAW_NM, slsp.OUT_BF16_NM, slsp.OUT_BF16_MN):
+                kw = {} if mode == slsp.OUT_RAW_NM else {"s_ch": s_ch, "s_tok": s_tok}
+                outs[(tag, mode)] = slsp.sparse_gemm(pw, payload, out_mode=mode, **kw)
+    torch.cuda.synchronize()
+    for mode in (slsp.OUT_RAW_NM, slsp.OUT_BF16_NM, slsp.OUT_BF16_MN):
+        a, b = outs[("cl", mode)], outs[("ws", mode)]
+        iv = torch.int16 if a.element_size() == 2 else torch.int32
+        assert torch.equal(a.view(iv), b.view(iv)), mode
